@@ -1,0 +1,272 @@
+"""Benchmark: active-batch particles/s on HM-large depleted fuel (C4).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU, NCCL)
+
+Workload (BASELINE.json configs[3], SURVEY.md section 8 "C4"): library
+depleted_pincell(272 fuel, 3 moderator, 11303 grid points, 100 axial) seed 1,
+k-eigenvalue, event mode, sorted lookups, fused tallies, fast (atomic)
+reduction, 40M particles per GPU per batch (weak scaling: ppb = N x 40M).
+A step is one active batch; W warm-up batches (inactive: batch 0 samples the
+source from scratch, later ones resample the bank) precede K timed active
+batches.  The library (99.5 MB of grid records) is resident in HBM and every
+batch re-reads it >100x over through ~40M x 10.5 lookups, so inputs are far
+larger than L2 in aggregate traffic; no flush between batches is needed.
+
+value     = K*ppb / device time of the K active batches (CUDA events on the
+            engine stream, max over ranks)
+e2e       = RunResult.active_rate of the same run_event() call: the
+            reference's own metric definition (replication.py:282-304, host
+            wall per batch incl. host merge/reduce/resample and the per-batch
+            D2H of counters/tallies), i.e. through the public API.
+roofline  = XS-lookup kernel: algorithmic bytes = 64 B per (lookup, nuclide)
+            (grid pair + sigma_t/c/f pairs) / summed k_lookup time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particles/s (active batches), HM-large depleted fuel, at 1/2/4/8 B200"
+WORKLOAD = dict(workload="C4 HM-large depleted pincell: depleted_pincell(272,3,11303,100,seed=1)",
+                ppb_per_gpu=40_000_000, mode="event", reduction="fast", tally_mode="fused",
+                sort="on (mat, log E) every lookup sweep", seed=42)
+BYTES_PER_NUCLIDE_LOOKUP = 64
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--format=csv,noheader,nounits",
+                                      f"--query-gpu={self.FIELDS}"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in self.rows:
+            for name, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+def init_dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws <= 1:
+        return 0, 1, 0
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, ws, local
+
+
+def cpu_baseline(lib, cell, threads: int, ppb_sample: int, batches=(1, 2)) -> dict:
+    """The C oracle (restatement of the reference kernels, pinned bit-exact to
+    it) on this host's cores, W workers like run_replicated."""
+    from oracle import driver
+    cfg = dict(particles_per_batch=ppb_sample, inactive_batches=batches[0],
+               active_batches=batches[1], mode="event", max_in_flight=10000,
+               tally_mode="fused", reduction="deterministic", sort_enabled=True,
+               sort_every_n=1, seed=42, workers=threads)
+    res = driver.run(cfg, lib.arrays(), cell.as_tuple(), workers=threads)
+    return dict(value=res["active_rate"], unit="particles/s", cores=threads, kind="port",
+                sample=f"C4 library, {ppb_sample} particles/batch x ({batches[0]} inactive + "
+                       f"{batches[1]} active), event mode, {threads} worker threads, "
+                       f"deterministic reduction (reference defaults)")
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (oracle port; the reference
+    is Python/numba and cannot travel to the GPU box) on all host cores."""
+    rank, ws, _ = init_dist()
+    if rank != 0:
+        return
+    from paper_2403_12345_b200.presets import depleted_pincell
+    lib, cell = depleted_pincell(272, 3, 11303, 100, seed=1)
+    threads = os.cpu_count() or 1
+    ppb = args.ref_particles or 1500 * threads
+    from oracle import driver
+    cfg = dict(particles_per_batch=ppb, inactive_batches=args.warmup, active_batches=args.steps,
+               mode="event", max_in_flight=10000, tally_mode="fused", reduction="deterministic",
+               sort_enabled=True, sort_every_n=1, seed=42, workers=threads)
+    res = driver.run(cfg, lib.arrays(), cell.as_tuple(), workers=threads)
+    v = res["active_rate"]
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "particles/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * res["active_wall"] / max(args.steps, 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": dict(WORKLOAD, ppb_sample=ppb),
+            "cpu_baseline": {"value": v, "unit": "particles/s", "cores": threads, "kind": "port",
+                             "sample": f"{ppb} particles/batch x ({args.warmup}+{args.steps}) batches"},
+            "e2e": {"value": v, "unit": "particles/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    rank, ws, local = init_dist()
+    import paper_2403_12345_b200 as P
+    from paper_2403_12345_b200 import replication
+    from paper_2403_12345_b200.distributed import current_world
+
+    t0 = time.perf_counter()
+    lib, cell = P.depleted_pincell(272, 3, 11303, 100, seed=1)
+    t_lib = time.perf_counter() - t0
+    ppb_gpu = args.particles
+    cfg = P.RunConfig(particles_per_batch=ppb_gpu * ws, inactive_batches=args.warmup,
+                      active_batches=args.steps, mode="event", sort_enabled=True,
+                      max_in_flight=args.max_in_flight or ppb_gpu, tally_mode="fused",
+                      reduction="fast", seed=42, workers=ws)
+    dev = torch.cuda.current_device()
+    eng = replication.engine_for(dev, lib, cell)
+    stream = torch.cuda.current_stream()
+    eng.set_stream(stream.cuda_stream)
+    ev = {}
+    launches0 = {}
+    sampler = ClockSampler(local)
+
+    def on_batch(b, phase, e):
+        if b == args.warmup and phase == "start":
+            if ws > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            sampler.__enter__()
+            ev["start"] = torch.cuda.Event(enable_timing=True)
+            ev["start"].record(stream)
+            launches0["n"] = e.launch_count
+        if b == args.warmup + args.steps - 1 and phase == "end":
+            ev["end"] = torch.cuda.Event(enable_timing=True)
+            ev["end"].record(stream)
+            torch.cuda.synchronize()
+            launches0["end"] = e.launch_count
+            sampler.__exit__()
+
+    res = P.run_event(cfg, lib, cell, on_batch=on_batch)
+    dev_ms = ev["start"].elapsed_time(ev["end"])
+    if ws > 1:
+        t = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dev_ms = float(t.item())
+    value = args.steps * cfg.particles_per_batch / (dev_ms * 1e-3)
+    if rank != 0:
+        return
+    # roofline of the XS-lookup kernel (timings are summed over ranks; per-rank mean)
+    n_nl = res.timings["nuclide_lookups_active"]
+    peak, peak_src = _peaks()
+    lk_time = res.timings["lookup_active_s"] / ws if "lookup_active_s" in res.timings else None
+    achieved = (BYTES_PER_NUCLIDE_LOOKUP * n_nl / ws) / lk_time / 1e9 if lk_time else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_lookup_summary.json")) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_nuclide_lookup")
+        if traffic is not None:
+            traffic = traffic * (n_nl / ws) / max(1, res.timings.get("lookup_launches_active", 1) / ws)
+    except Exception:  # noqa: BLE001
+        traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": dict(WORKLOAD, global_batch=cfg.particles_per_batch,
+                       parallelism=f"domain replication x{ws}", l2="inputs >> L2 in traffic; no flush",
+                       library_build_s=round(t_lib, 2)),
+        "e2e": {"value": res.active_rate, "unit": "particles/s",
+                "h2d_bytes_per_step": res.timings.get("h2d_bytes_active", 0) / max(args.steps, 1),
+                "d2h_bytes_per_step": res.timings.get("d2h_bytes_active", 0) / max(args.steps, 1)},
+        "gpu_launches": int(launches0["end"] - launches0["n"]),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "kernel": "k_lookup", "peak_source": peak_src,
+                     "algorithmic_bytes": "64 B x nuclide-lookups (grid pair + sigma_t,c,f pairs)",
+                     "nuclide_lookups_per_step": n_nl / args.steps},
+        "clocks": sampler.summary(),
+        "k_mean": res.k_mean, "k_stderr": res.k_stderr,
+        "timings_s": {k: v for k, v in res.timings.items() if isinstance(v, float)},
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        line["cpu_baseline"] = cpu_baseline(lib, cell, threads, args.cpu_particles or 1000 * threads)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--particles", type=int, default=40_000_000, help="particles per GPU per batch")
+    ap.add_argument("--max-in-flight", type=int, default=0)
+    ap.add_argument("--cpu-particles", type=int, default=0)
+    ap.add_argument("--ref-particles", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

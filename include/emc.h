@@ -1,0 +1,168 @@
+/* emc.h -- C ABI of libemc.so, the B200 (sm_100a) event-based Monte Carlo
+ * transport engine.  Plain pointers and sizes only; no torch types.
+ *
+ * Every entry point replaces one compiled-kernel call of the reference
+ * package eventmc (/root/reference/pkg/src/eventmc); the reference's Python
+ * layer reaches those kernels through numba dispatch, so the "FFI" this ABI
+ * stands in for is the argument tuple of each @njit function.  The binding a
+ * maintainer adds on the reference side is shown in INTEGRATION.md.
+ *
+ * Ownership: the context owns every device buffer (library, geometry,
+ * particle slots, queues, fission bank, contribution log); callers own host
+ * buffers and pass them in/out.  All calls are synchronous w.r.t. the host
+ * unless stated, run on the stream set by emc_set_stream (default: the
+ * legacy stream), and return 0 on success or a negative EMC_E_* code; the
+ * message is in emc_last_error().  Transport errors detected on the device use
+ * the reference's codes (kernels.py:108-113) in emc_batch_result.error.
+ */
+#ifndef EMC_H
+#define EMC_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EMC_ABI_VERSION 1
+#define EMC_N_COUNTERS 24   /* kernels.py:81-103 layout */
+#define EMC_N_TIMINGS 4     /* kernels.py:115-120: lookup, advance, collision, sort */
+
+enum {
+    EMC_OK = 0,
+    EMC_E_CUDA = -1,       /* CUDA runtime failure */
+    EMC_E_ARG = -2,        /* invalid argument / call order */
+    EMC_E_OOM = -3,        /* device allocation failed */
+    EMC_E_RANGE = -4       /* problem exceeds an encoding limit */
+};
+
+/* transport error codes (kernels.py:108-113) */
+enum { EMC_ERR_NO_SURFACE = 1, EMC_ERR_OUTSIDE_BOX = 2, EMC_ERR_STREAM_OVERLAP = 3,
+       EMC_ERR_RUNAWAY_HISTORY = 4, EMC_ERR_QUEUE_STATE = 5, EMC_ERR_NONPOSITIVE_SIGMA = 6 };
+
+typedef struct emc_ctx emc_ctx;
+
+/* Library.arrays() (xslib.py:119-153): nuclide grids + channels, material
+ * compositions, global energy bounds. */
+typedef struct {
+    int64_t n_nuclides, n_points, n_materials, n_entries;
+    const int64_t *grid_off;                 /* [n_nuclides+1] */
+    const double *grids, *ch_t, *ch_s, *ch_c, *ch_f; /* [n_points] */
+    const double *nu;                        /* [n_nuclides] */
+    const int64_t *mat_off;                  /* [n_materials+1] */
+    const int32_t *mat_nuc;                  /* [n_entries] */
+    const double *mat_den;                   /* [n_entries] */
+    double emin, emax;
+} emc_library;
+
+/* Pincell.as_tuple() (geometry.py:83-90) */
+typedef struct {
+    double radius, r2, half_pitch, height;
+    int64_t n_axial;
+    const double *zplanes;                   /* [n_axial+1] */
+    const int32_t *fuel_mats;                /* [n_axial] */
+    int64_t mod_mat;
+} emc_geometry;
+
+/* RunConfig (transport.py:26-99) restricted to what the engine consumes, plus
+ * this rank's contiguous block of particle indices [gid_lo, gid_lo+n_assigned). */
+typedef struct {
+    int64_t particles_per_batch;             /* pmax in the stream layout */
+    int64_t gid_lo, n_assigned;
+    int64_t max_in_flight;
+    int32_t history;                         /* 1: history-based executor */
+    int32_t fused;                           /* tally_mode == "fused" */
+    int32_t use_logs;                        /* reduction == "deterministic" */
+    int32_t sort_enabled, sort_every;
+    int32_t pad;
+    uint64_t seed;
+    double alpha, fission_t;
+    int64_t perturb_gid;                     /* -1: none */
+} emc_run_config;
+
+typedef struct {
+    int64_t batch;
+    double k_run;
+    int32_t batch0, score;                   /* score = active batch */
+} emc_batch_args;
+
+typedef struct {
+    int64_t counters[EMC_N_COUNTERS];
+    double timings[EMC_N_TIMINGS];           /* seconds, CUDA events */
+    int64_t n_sites, n_logs, iterations, launches;
+    int32_t error;                           /* EMC_ERR_* or 0 */
+    int32_t reruns;                          /* overflow grow-and-rerun count (R:122-142) */
+    int64_t error_gid;
+} emc_batch_result;
+
+const char *emc_last_error(void);
+int emc_abi_version(void);
+int emc_device_count(int *n);
+
+int emc_create(int device, emc_ctx **out);
+void emc_destroy(emc_ctx *ctx);
+/* use an existing cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream) */
+int emc_set_stream(emc_ctx *ctx, void *cuda_stream);
+
+/* replaces the lib tuple built at replication.py:169 */
+int emc_upload_library(emc_ctx *ctx, const emc_library *lib);
+/* replaces the geom tuple built at replication.py:171 */
+int emc_upload_geometry(emc_ctx *ctx, const emc_geometry *geom);
+/* replaces _Worker allocation (replication.py:62-111) */
+int emc_configure(emc_ctx *ctx, const emc_run_config *cfg);
+
+/* source of batch b>0: systematic resampling (transport.py:188-200) with
+ * uniform u of the canonical bank of batch b-1 -- either this context's own
+ * bank (single rank) or a device-resident global bank (multi-rank, 7 arrays
+ * x,y,z,dx,dy,dz,E of length n that stay valid during the next batch) */
+int emc_set_source_local(emc_ctx *ctx, double u);
+int emc_set_source_device(emc_ctx *ctx, const void *const ptrs[7], int64_t n, double u);
+
+/* one worker-batch: replaces kernels.run_event_batch / run_history_batch
+ * (kernels.py:1043-1211) as called at replication.py:127-138, including the
+ * grow-and-rerun on buffer overflow.  Leaves the canonical (parent, ordinal)
+ * sorted fission bank of this rank on the device. */
+int emc_run_batch(emc_ctx *ctx, const emc_batch_args *args, emc_batch_result *res);
+
+/* batch sums of this rank (tally.py:66-93): deterministic mode folds the
+ * contribution log in canonical order starting from init (NULL = zeros; a
+ * previous rank's partial sums to chain ranks bit-exactly); fast mode returns
+ * the atomically accumulated bins (+init). */
+int emc_reduce_bins(emc_ctx *ctx, const double *init, double *out, int64_t n_bins);
+
+/* canonical bank of the last batch */
+int emc_bank_size(emc_ctx *ctx, int64_t *n);
+int emc_bank_device(emc_ctx *ctx, void *ptrs[9]);  /* parent,ord,x,y,z,dx,dy,dz,E */
+int emc_bank_copy(emc_ctx *ctx, int64_t start, int64_t n, int64_t *parent, int32_t *ord,
+                  double *x, double *y, double *z, double *dx, double *dy, double *dz,
+                  double *E);
+
+/* --- single-operation entry points (public API wrappers) --- */
+/* kernels.macro_lookup_full (kernels.py:287-331): sums[n][5], partials[n][max_comp][4] (nullable) */
+int emc_xs_lookup(emc_ctx *ctx, int64_t n, const int32_t *mats, const double *E, double *sums,
+                  double *partials, int32_t max_comp);
+/* kernels.locate_point (kernels.py:403-415): out[n][3] = kind, axial, material */
+int emc_locate(emc_ctx *ctx, int64_t n, const double *pos, int32_t *out);
+/* kernels.boundary_distance (kernels.py:418-492): cell[n][2] = kind, axial */
+int emc_distance(emc_ctx *ctx, int64_t n, const double *pos, const double *dir,
+                 const int32_t *cell, double *dist, int32_t *surf);
+/* transport.sample_isotropic / sample_collision_distance (transport.py:161-174) */
+int emc_particle_ops(emc_ctx *ctx, int64_t n, const uint64_t *states, const double *sigma_t,
+                     double *iso, double *dcol, uint64_t *state_iso, uint64_t *state_dcol);
+/* kernels.sort_queue (kernels.py:1014-1035): stable sort of q by (mat[q], E[q]) */
+int emc_sort_queue(emc_ctx *ctx, int64_t n, const int32_t *q, int64_t n_slots,
+                   const int32_t *mat, const double *E, int32_t *out);
+/* kernels.replay_into_bins (kernels.py:1219-1223): sums[b] += vals in order */
+int emc_replay_bins(emc_ctx *ctx, int64_t n, const int32_t *bin, const double *val,
+                    int32_t n_bins, double *sums);
+/* kernels.lcg_skip (kernels.py:144-158) */
+int emc_lcg_skip(emc_ctx *ctx, int64_t n, const uint64_t *state, const uint64_t *k, uint64_t *out);
+/* device log/sin/cos replicas (emc_libm.h): out[n][3] */
+int emc_libm_eval(emc_ctx *ctx, int64_t n, const double *x, double *out);
+
+/* number of kernel launches issued by this context so far */
+int64_t emc_launch_count(emc_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EMC_H */

@@ -1,0 +1,891 @@
+// libemc.so: host side of the B200 transport engine and its C ABI (include/emc.h).
+//
+// One emc_ctx per GPU (one process per GPU under torch.distributed).  The
+// context owns the device library (interleaved grid records + log-hash
+// bracket table), the particle slots (SoA), the event queues, the fission
+// bank and the contribution log, and drives the event loop of one batch:
+//
+//   source_init -> { [sort] -> lookup -> advance -> crossing | collision(+refill) }*
+//   -> canonical bank sort -> (deterministic) log sort
+//
+// Reference: replication.py:114-142 (_run_worker_batch) and kernels.py:1092-1211.
+#include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/emc.h"
+#include "emc_aux_kernels.cuh"
+#include "emc_history.cuh"
+#include "emc_kernels.cuh"
+
+using namespace emc;
+
+static thread_local std::string g_err;
+
+#define EMC_TRY_CUDA(expr)                                                             \
+    do {                                                                               \
+        cudaError_t e_ = (expr);                                                       \
+        if (e_ != cudaSuccess) {                                                       \
+            g_err = std::string(#expr) + ": " + cudaGetErrorString(e_);                \
+            return EMC_E_CUDA;                                                         \
+        }                                                                              \
+    } while (0)
+
+#define EMC_CHECK_LAUNCH(ctx)                                                          \
+    do {                                                                               \
+        (ctx)->launches++;                                                             \
+        cudaError_t e_ = cudaGetLastError();                                           \
+        if (e_ != cudaSuccess) {                                                       \
+            g_err = std::string("kernel launch: ") + cudaGetErrorString(e_);           \
+            return EMC_E_CUDA;                                                         \
+        }                                                                              \
+    } while (0)
+
+static int fail_arg(const char* msg) { g_err = msg; return EMC_E_ARG; }
+
+namespace {
+
+// device buffer with typed pointer; realloc drops contents
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    int alloc(size_t count) {
+        if (count <= n && p) return 0;
+        if (p) cudaFree(p);
+        p = nullptr; n = 0;
+        if (count == 0) return 0;
+        if (cudaMalloc(&p, count * sizeof(T)) != cudaSuccess) {
+            cudaGetLastError();
+            g_err = "cudaMalloc failed (" + std::to_string(count * sizeof(T)) + " bytes)";
+            return EMC_E_OOM;
+        }
+        n = count;
+        return 0;
+    }
+    void release() { if (p) cudaFree(p); p = nullptr; n = 0; }
+};
+
+struct SiteBufs {
+    DBuf<int64_t> parent; DBuf<int32_t> ord;
+    DBuf<double> x, y, z, dx, dy, dz, E;
+    int alloc(size_t cap) {
+        int rc = 0;
+        rc |= parent.alloc(cap); rc |= ord.alloc(cap);
+        rc |= x.alloc(cap); rc |= y.alloc(cap); rc |= z.alloc(cap);
+        rc |= dx.alloc(cap); rc |= dy.alloc(cap); rc |= dz.alloc(cap); rc |= E.alloc(cap);
+        return rc ? EMC_E_OOM : 0;
+    }
+    DSites view() const {
+        return DSites{parent.p, ord.p, x.p, y.p, z.p, dx.p, dy.p, dz.p, E.p, (int64_t)parent.n};
+    }
+    void release() {
+        parent.release(); ord.release(); x.release(); y.release(); z.release();
+        dx.release(); dy.release(); dz.release(); E.release();
+    }
+};
+
+inline int grid_for(int64_t n, int block, int max_blocks)
+{
+    int64_t b = (n + block - 1) / block;
+    if (b < 1) b = 1;
+    return (int)std::min<int64_t>(b, max_blocks);
+}
+
+}  // namespace
+
+struct emc_ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t stream = nullptr;
+    int64_t launches = 0;
+
+    // library
+    bool have_lib = false;
+    DBuf<Rec> rec; DBuf<double> ch_s, nu; DBuf<int32_t> mat_off; DBuf<Comp> comp; DBuf<int32_t> hash;
+    DLib L{};
+    int32_t n_materials = 0, max_comp = 0;
+    int64_t lib_bytes = 0;
+
+    // geometry
+    bool have_geom = false;
+    DBuf<double> zplanes; DBuf<int32_t> fuel_mats;
+    DGeom G{};
+
+    // run configuration
+    bool configured = false;
+    emc_run_config cfg{};
+    int64_t nslots = 0;
+    int32_t nck = 0, n_bins = 0, kbin = 0, e_bits = 20, mat_bits = 1;
+
+    // particle slots
+    DBuf<double> px, py, pz, dx, dy, dz, en, cm_t, cm_c, cm_f, cm_nsf, ckpt;
+    DBuf<uint64_t> rng; DBuf<int32_t> draws, ordctr, histlog, axial, mat, surf; DBuf<int64_t> gid;
+    DBuf<int8_t> kind;
+    DSlots S{};
+
+    // queues + sort scratch
+    DBuf<int32_t> qa, qb, qs, qc, qx;
+    DBuf<uint32_t> keys_in, keys_out;
+    DBuf<unsigned char> cub_tmp;
+
+    // fission bank: raw appends + canonical (sorted) copy
+    // two canonical-bank buffers: batch b reads bank[cur] (its source, when
+    // local) and writes its own canonical bank into bank[1-cur]
+    SiteBufs sites, banks[2];
+    int cur_bank = 0;
+    int64_t bank_n = 0;
+    SiteBufs& bank() { return banks[cur_bank]; }
+    DBuf<uint64_t> bkey_in, bkey_out; DBuf<int32_t> bidx_in, bidx_out;
+
+    // contribution log
+    DBuf<int64_t> lg_gid; DBuf<int32_t> lg_ord, lg_bin; DBuf<double> lg_val;
+    int64_t log_n = 0;
+    DBuf<uint64_t> lkey_in, lkey_out; DBuf<double> lval_out;
+    int gid_bits = 1;
+
+    // per batch
+    DBuf<double> bins, bins_init, bins_out; DBuf<unsigned long long> cnt; DBuf<Ctl> ctl;
+    Ctl* ctl_host = nullptr;
+    DSrc src{};
+    cudaEvent_t ev[16]{};
+    bool ev_init = false;
+};
+
+// ------------------------------------------------------------------ misc ---
+
+extern "C" const char* emc_last_error(void) { return g_err.c_str(); }
+extern "C" int emc_abi_version(void) { return EMC_ABI_VERSION; }
+
+extern "C" int emc_device_count(int* n)
+{
+    EMC_TRY_CUDA(cudaGetDeviceCount(n));
+    return 0;
+}
+
+extern "C" int emc_create(int device, emc_ctx** out)
+{
+    if (!out) return fail_arg("emc_create: out is NULL");
+    EMC_TRY_CUDA(cudaSetDevice(device));
+    emc_ctx* c = new emc_ctx();
+    c->device = device;
+    cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (cudaMallocHost(&c->ctl_host, sizeof(Ctl)) != cudaSuccess) { delete c; g_err = "cudaMallocHost"; return EMC_E_CUDA; }
+    if (c->ctl.alloc(1) || c->cnt.alloc(EMC_N_COUNTERS)) { delete c; return EMC_E_OOM; }
+    for (auto& e : c->ev) cudaEventCreate(&e);
+    c->ev_init = true;
+    *out = c;
+    return 0;
+}
+
+extern "C" void emc_destroy(emc_ctx* c)
+{
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (auto* b : {&c->px, &c->py, &c->pz, &c->dx, &c->dy, &c->dz, &c->en, &c->cm_t, &c->cm_c, &c->cm_f,
+                    &c->cm_nsf, &c->ckpt, &c->ch_s, &c->nu, &c->zplanes, &c->bins, &c->bins_init,
+                    &c->bins_out, &c->lg_val, &c->lval_out})
+        b->release();
+    for (auto* b : {&c->draws, &c->ordctr, &c->histlog, &c->axial, &c->mat, &c->surf, &c->mat_off, &c->hash,
+                    &c->fuel_mats, &c->qa, &c->qb, &c->qs, &c->qc, &c->qx, &c->bidx_in, &c->bidx_out,
+                    &c->lg_ord, &c->lg_bin})
+        b->release();
+    c->rng.release(); c->gid.release(); c->kind.release(); c->rec.release(); c->comp.release();
+    c->keys_in.release(); c->keys_out.release(); c->cub_tmp.release();
+    c->bkey_in.release(); c->bkey_out.release(); c->lkey_in.release(); c->lkey_out.release();
+    c->lg_gid.release(); c->cnt.release(); c->ctl.release();
+    c->sites.release(); c->banks[0].release(); c->banks[1].release();
+    if (c->ctl_host) cudaFreeHost(c->ctl_host);
+    if (c->ev_init) for (auto& e : c->ev) cudaEventDestroy(e);
+    delete c;
+}
+
+extern "C" int emc_set_stream(emc_ctx* c, void* stream)
+{
+    if (!c) return fail_arg("null ctx");
+    c->stream = (cudaStream_t)stream;
+    return 0;
+}
+
+extern "C" int64_t emc_launch_count(emc_ctx* c) { return c ? c->launches : -1; }
+
+// --------------------------------------------------------------- library ---
+
+extern "C" int emc_upload_library(emc_ctx* c, const emc_library* lib)
+{
+    if (!c || !lib) return fail_arg("emc_upload_library: null argument");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    const int64_t nn = lib->n_nuclides, np = lib->n_points, nm = lib->n_materials, ne = lib->n_entries;
+    if (nn < 1 || nm < 1 || np < 1) return fail_arg("empty library");
+    if (np > INT32_MAX / 2 || ne > INT32_MAX / 2) { g_err = "library too large for 32-bit indices"; return EMC_E_RANGE; }
+    for (int64_t i = 0; i < nn; ++i)
+        if (lib->grid_off[i + 1] - lib->grid_off[i] < 1) return fail_arg("nuclide with an empty grid");
+
+    // interleaved {E, t, c, f} records
+    std::vector<Rec> hrec(np);
+    for (int64_t i = 0; i < np; ++i) hrec[i] = Rec{lib->grids[i], lib->ch_t[i], lib->ch_c[i], lib->ch_f[i]};
+
+    // composition entries, with den*nu formed exactly as the reference does
+    std::vector<Comp> hcomp(std::max<int64_t>(ne, 1));
+    std::vector<int32_t> hmo(nm + 1);
+    int32_t maxc = 0;
+    for (int64_t m = 0; m <= nm; ++m) hmo[m] = (int32_t)lib->mat_off[m];
+    for (int64_t m = 0; m < nm; ++m) maxc = std::max<int32_t>(maxc, (int32_t)(lib->mat_off[m + 1] - lib->mat_off[m]));
+    for (int64_t k = 0; k < ne; ++k) {
+        int32_t nid = lib->mat_nuc[k];
+        if (nid < 0 || nid >= nn) return fail_arg("composition references an unknown nuclide");
+        volatile double dn = lib->mat_den[k] * lib->nu[nid];
+        hcomp[k] = Comp{lib->mat_den[k], (double)dn, (int32_t)lib->grid_off[nid],
+                        (int32_t)(lib->grid_off[nid + 1] - lib->grid_off[nid]), nid, 0};
+    }
+
+    // log-hash: bins are (bits(E) >> shift); 2^m bins per octave with 2^m >=
+    // the densest grid's points per octave.
+    double lo = lib->emin, hi = lib->emax;
+    if (!(lo > 0.0) || !(hi >= lo)) return fail_arg("library energy bounds must be positive");
+    int64_t gmax = 1;
+    for (int64_t i = 0; i < nn; ++i) gmax = std::max<int64_t>(gmax, lib->grid_off[i + 1] - lib->grid_off[i]);
+    double octaves = std::max(1.0, std::log2(hi / lo));
+    int mbits = (int)std::ceil(std::log2(std::max(1.0, (double)gmax / octaves)));
+    mbits = std::min(std::max(mbits, 0), 16);
+    int shift = 52 - mbits;
+    uint64_t blo, bhi;
+    std::memcpy(&blo, &lo, 8); std::memcpy(&bhi, &hi, 8);
+    int64_t key_lo = (int64_t)(blo >> shift), key_hi = (int64_t)(bhi >> shift);
+    int64_t nbins = key_hi - key_lo + 1;
+    if (nbins * nn > (int64_t)1 << 31) { g_err = "hash table too large"; return EMC_E_RANGE; }
+    std::vector<int32_t> hhash(nbins * nn);
+    for (int64_t nid = 0; nid < nn; ++nid) {
+        const double* gr = lib->grids + lib->grid_off[nid];
+        int64_t G = lib->grid_off[nid + 1] - lib->grid_off[nid];
+        int64_t j = 0;   // number of grid points <= current bin's lower edge
+        for (int64_t b = 0; b < nbins; ++b) {
+            uint64_t eb = (uint64_t)(key_lo + b) << shift;
+            double edge;
+            std::memcpy(&edge, &eb, 8);
+            while (j < G && gr[j] <= edge) ++j;
+            int64_t start = j - 1;                       // searchsorted(right) - 1
+            if (start < 0) start = 0;
+            if (b == 0) start = 0;
+            if (G >= 2 && start > G - 2) start = G - 2;
+            if (G < 2) start = 0;
+            hhash[nid * nbins + b] = (int32_t)start;
+        }
+    }
+
+    int rc = 0;
+    rc |= c->rec.alloc(np); rc |= c->ch_s.alloc(np); rc |= c->nu.alloc(nn); rc |= c->mat_off.alloc(nm + 1);
+    rc |= c->comp.alloc(hcomp.size()); rc |= c->hash.alloc(hhash.size());
+    if (rc) return EMC_E_OOM;
+    EMC_TRY_CUDA(cudaMemcpy(c->rec.p, hrec.data(), np * sizeof(Rec), cudaMemcpyHostToDevice));
+    EMC_TRY_CUDA(cudaMemcpy(c->ch_s.p, lib->ch_s, np * sizeof(double), cudaMemcpyHostToDevice));
+    EMC_TRY_CUDA(cudaMemcpy(c->nu.p, lib->nu, nn * sizeof(double), cudaMemcpyHostToDevice));
+    EMC_TRY_CUDA(cudaMemcpy(c->mat_off.p, hmo.data(), (nm + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
+    EMC_TRY_CUDA(cudaMemcpy(c->comp.p, hcomp.data(), hcomp.size() * sizeof(Comp), cudaMemcpyHostToDevice));
+    EMC_TRY_CUDA(cudaMemcpy(c->hash.p, hhash.data(), hhash.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    c->L = DLib{c->rec.p, c->ch_s.p, c->nu.p, c->mat_off.p, c->comp.p, c->hash.p, key_lo, (int32_t)nbins,
+                shift, lo, hi};
+    c->n_materials = (int32_t)nm;
+    c->max_comp = maxc;
+    c->lib_bytes = (int64_t)(np * (sizeof(Rec) + 8) + hcomp.size() * sizeof(Comp) + hhash.size() * 4);
+    c->have_lib = true;
+    return 0;
+}
+
+extern "C" int emc_upload_geometry(emc_ctx* c, const emc_geometry* g)
+{
+    if (!c || !g) return fail_arg("emc_upload_geometry: null argument");
+    if (g->n_axial < 1) return fail_arg("n_axial must be >= 1");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    if (c->zplanes.alloc(g->n_axial + 1) || c->fuel_mats.alloc(g->n_axial)) return EMC_E_OOM;
+    EMC_TRY_CUDA(cudaMemcpy(c->zplanes.p, g->zplanes, (g->n_axial + 1) * 8, cudaMemcpyHostToDevice));
+    EMC_TRY_CUDA(cudaMemcpy(c->fuel_mats.p, g->fuel_mats, g->n_axial * 4, cudaMemcpyHostToDevice));
+    c->G = DGeom{g->radius, g->r2, g->half_pitch, g->height, (int32_t)g->n_axial, (int32_t)g->mod_mat,
+                 c->zplanes.p, c->fuel_mats.p};
+    c->n_bins = (int32_t)((g->n_axial + 1) * 5 + 1);
+    c->kbin = c->n_bins - 1;
+    c->have_geom = true;
+    return 0;
+}
+
+// -------------------------------------------------------------- configure ---
+
+static int alloc_sites(emc_ctx* c, size_t cap)
+{
+    // never touches banks[cur_bank]: it may be this batch's source
+    if (c->sites.alloc(cap) || c->banks[1 - c->cur_bank].alloc(cap)) return EMC_E_OOM;
+    if (c->bkey_in.alloc(cap) || c->bkey_out.alloc(cap) || c->bidx_in.alloc(cap) || c->bidx_out.alloc(cap))
+        return EMC_E_OOM;
+    return 0;
+}
+
+static int alloc_logs(emc_ctx* c, size_t cap)
+{
+    if (c->lg_gid.alloc(cap) || c->lg_ord.alloc(cap) || c->lg_bin.alloc(cap) || c->lg_val.alloc(cap)) return EMC_E_OOM;
+    if (c->lkey_in.alloc(cap) || c->lkey_out.alloc(cap) || c->lval_out.alloc(cap)) return EMC_E_OOM;
+    return 0;
+}
+
+extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
+{
+    if (!c || !cfg) return fail_arg("emc_configure: null argument");
+    if (!c->have_lib || !c->have_geom) return fail_arg("upload library and geometry before emc_configure");
+    if (cfg->n_assigned < 1 || cfg->max_in_flight < 1 || cfg->sort_every < 1) return fail_arg("bad run config");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    c->cfg = *cfg;
+    int64_t nslots = std::max<int64_t>(1, std::min<int64_t>(cfg->max_in_flight, cfg->n_assigned));
+    if (nslots > INT32_MAX / 2) { g_err = "max_in_flight too large"; return EMC_E_RANGE; }
+    c->nslots = nslots;
+    c->nck = cfg->fused ? std::max(0, (c->max_comp - 1) / kCkptStride) : 0;
+    int rc = 0;
+    for (auto* b : {&c->px, &c->py, &c->pz, &c->dx, &c->dy, &c->dz, &c->en, &c->cm_t, &c->cm_c, &c->cm_f, &c->cm_nsf})
+        rc |= b->alloc(nslots);
+    rc |= c->ckpt.alloc(std::max<int64_t>(1, (int64_t)c->nck * nslots));
+    rc |= c->rng.alloc(nslots); rc |= c->gid.alloc(nslots); rc |= c->kind.alloc(nslots);
+    for (auto* b : {&c->draws, &c->ordctr, &c->histlog, &c->axial, &c->mat, &c->surf, &c->qa, &c->qb, &c->qs, &c->qc, &c->qx})
+        rc |= b->alloc(nslots);
+    rc |= c->keys_in.alloc(nslots); rc |= c->keys_out.alloc(nslots);
+    rc |= c->bins.alloc(c->n_bins); rc |= c->bins_init.alloc(c->n_bins); rc |= c->bins_out.alloc(c->n_bins);
+    if (rc) return EMC_E_OOM;
+    c->S = DSlots{c->px.p, c->py.p, c->pz.p, c->dx.p, c->dy.p, c->dz.p, c->en.p, c->rng.p, c->draws.p,
+                  c->ordctr.p, c->histlog.p, c->axial.p, c->mat.p, c->surf.p, c->gid.p, c->kind.p,
+                  c->cm_t.p, c->cm_c.p, c->cm_f.p, c->cm_nsf.p, c->ckpt.p, nslots, c->nck};
+    // fission bank: reference starts at n_assigned*6+1024 (R:92); ~1 site per
+    // source particle is typical, so start at 2x and grow on overflow.
+    if ((rc = alloc_sites(c, (size_t)(cfg->n_assigned * 2 + 4096)))) return rc;
+    if (cfg->use_logs) {
+        if ((rc = alloc_logs(c, (size_t)(cfg->n_assigned * 64 + 4096)))) return rc;
+    }
+    // sort key: material bits + energy bits in 32 bits
+    int mb = 1;
+    while ((1 << mb) < c->n_materials) ++mb;
+    c->mat_bits = mb;
+    c->e_bits = std::min(22, 32 - mb);
+    int gb = 1;
+    while (((int64_t)1 << gb) < cfg->n_assigned) ++gb;
+    c->gid_bits = gb;
+    int bb = 1;
+    while ((1 << bb) < c->n_bins) ++bb;
+    if (bb + gb + 17 > 64) { g_err = "deterministic log key exceeds 64 bits"; return EMC_E_RANGE; }
+    // CUB scratch, sized for the largest sort we run
+    size_t t1 = 0, t2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint32_t*)nullptr, (uint32_t*)nullptr, (int32_t*)nullptr,
+                                    (int32_t*)nullptr, (int)nslots, 0, 32);
+    c->cub_tmp.alloc(std::max<size_t>(t1, 1));
+    (void)t2;
+    c->bank_n = 0;
+    c->src = DSrc{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.0};
+    c->configured = true;
+    return 0;
+}
+
+extern "C" int emc_set_source_local(emc_ctx* c, double u)
+{
+    if (!c || !c->configured) return fail_arg("not configured");
+    if (c->bank_n < 1) return fail_arg("no local bank to resample");
+    SiteBufs& b = c->bank();
+    c->src = DSrc{b.x.p, b.y.p, b.z.p, b.dx.p, b.dy.p, b.dz.p, b.E.p, c->bank_n, u};
+    return 0;
+}
+
+extern "C" int emc_set_source_device(emc_ctx* c, const void* const ptrs[7], int64_t n, double u)
+{
+    if (!c || !c->configured || !ptrs) return fail_arg("emc_set_source_device: bad arguments");
+    if (n < 1) return fail_arg("empty source bank");
+    c->src = DSrc{(const double*)ptrs[0], (const double*)ptrs[1], (const double*)ptrs[2], (const double*)ptrs[3],
+                  (const double*)ptrs[4], (const double*)ptrs[5], (const double*)ptrs[6], n, u};
+    return 0;
+}
+
+// ----------------------------------------------------------------- batch ---
+
+static int sort_cub(emc_ctx* c, const uint32_t* kin, uint32_t* kout, const int32_t* vin, int32_t* vout, int n,
+                    int end_bit)
+{
+    size_t need = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, need, kin, kout, vin, vout, n, 0, end_bit, c->stream);
+    if (need > c->cub_tmp.n && c->cub_tmp.alloc(need)) return EMC_E_OOM;
+    EMC_TRY_CUDA(cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, need, kin, kout, vin, vout, n, 0, end_bit, c->stream));
+    c->launches += 4;
+    return 0;
+}
+
+template <class K, class V>
+static int sort_cub64(emc_ctx* c, const K* kin, K* kout, const V* vin, V* vout, int64_t n, int end_bit)
+{
+    size_t need = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, need, kin, kout, vin, vout, (int)n, 0, end_bit, c->stream);
+    if (need > c->cub_tmp.n && c->cub_tmp.alloc(need)) return EMC_E_OOM;
+    EMC_TRY_CUDA(cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, need, kin, kout, vin, vout, (int)n, 0, end_bit,
+                                                 c->stream));
+    c->launches += (end_bit + 7) / 8;
+    return 0;
+}
+
+static int bits_for(int64_t v)
+{
+    int b = 1;
+    while (b < 63 && ((int64_t)1 << b) <= v) ++b;
+    return b;
+}
+
+// one attempt at a batch; returns 0 and fills res (res->error may be set)
+static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result* res)
+{
+    const emc_run_config& cf = c->cfg;
+    cudaStream_t st = c->stream;
+    BatchP bp{};
+    bp.seed = cf.seed & kLcgMask;
+    bp.batch = a->batch; bp.pmax = cf.particles_per_batch; bp.g_lo = cf.gid_lo; bp.n_assigned = cf.n_assigned;
+    bp.perturb_gid = cf.perturb_gid; bp.alpha = cf.alpha; bp.fission_t = cf.fission_t; bp.k_run = a->k_run;
+    bp.fused = cf.fused; bp.score = a->score; bp.use_logs = cf.use_logs; bp.batch0 = a->batch0;
+    bp.kbin = c->kbin; bp.history = cf.history;
+    if (!a->batch0 && (c->src.n < 1 || !c->src.x)) return fail_arg("batch > 0 needs a source bank (emc_set_source_*)");
+
+    DSites sv = c->sites.view();
+    DLog lg{c->lg_gid.p, c->lg_ord.p, c->lg_bin.p, c->lg_val.p, (int64_t)c->lg_gid.n};
+
+    EMC_TRY_CUDA(cudaMemsetAsync(c->cnt.p, 0, EMC_N_COUNTERS * sizeof(unsigned long long), st));
+    EMC_TRY_CUDA(cudaMemsetAsync(c->bins.p, 0, c->n_bins * sizeof(double), st));
+    Ctl z{};
+    const int64_t n0 = std::min<int64_t>(c->nslots, cf.n_assigned);
+    z.cursor = (unsigned long long)n0;
+    EMC_TRY_CUDA(cudaMemcpyAsync(c->ctl.p, &z, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+
+    int64_t host_cnt[EMC_N_COUNTERS] = {0};
+    double tm[4] = {0, 0, 0, 0};
+    int64_t iterations = 0;
+    const int BLK = 256;
+    const int maxb = c->sm_count * 16;
+
+    if (cf.history) {
+        // history executor: one thread per in-flight history (K:1043-1089)
+        z.cursor = 0;
+        EMC_TRY_CUDA(cudaMemcpyAsync(c->ctl.p, &z, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+        EMC_TRY_CUDA(cudaEventRecord(c->ev[0], st));
+        int64_t nthr = n0;
+        k_history<<<(unsigned)((nthr + 127) / 128), 128, 0, st>>>(bp, c->L, c->G, c->src, c->S, lg, sv, c->bins.p,
+                                                                   c->ctl.p, c->cnt.p, nthr);
+        EMC_CHECK_LAUNCH(c);
+        EMC_TRY_CUDA(cudaEventRecord(c->ev[1], st));
+        EMC_TRY_CUDA(cudaMemcpyAsync(c->ctl_host, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        EMC_TRY_CUDA(cudaStreamSynchronize(st));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+        tm[0] = ms * 1e-3;
+        host_cnt[CNT_MAX_INFLIGHT] = nthr;
+        iterations = 1;
+    } else {
+        int32_t* cur = c->qa.p;
+        int32_t* nxt = c->qb.p;
+        k_source_init<<<grid_for(n0, BLK, maxb), BLK, 0, st>>>(bp, c->L, c->G, c->src, c->S, (int32_t)n0, cur,
+                                                               c->ctl.p, c->cnt.p);
+        EMC_CHECK_LAUNCH(c);
+        EMC_TRY_CUDA(cudaMemcpyAsync(c->ctl_host, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        EMC_TRY_CUDA(cudaStreamSynchronize(st));
+        int64_t nL = c->ctl_host->nL2;
+        int64_t look_inv = 0;
+        float ms;
+        while (nL > 0 && c->ctl_host->err == 0) {
+            const int32_t* q = cur;
+            EMC_TRY_CUDA(cudaMemsetAsync(&c->ctl.p->nL2, 0, 3 * sizeof(unsigned), st));
+            bool do_sort = cf.sort_enabled && nL > 1 && (look_inv % cf.sort_every) == 0;
+            EMC_TRY_CUDA(cudaEventRecord(c->ev[0], st));
+            if (do_sort) {
+                k_sort_keys<<<grid_for(nL, BLK, 1 << 30), BLK, 0, st>>>(cur, (int32_t)nL, c->mat.p, c->en.p,
+                                                                        c->keys_in.p, c->e_bits);
+                EMC_CHECK_LAUNCH(c);
+                int rc = sort_cub(c, c->keys_in.p, c->keys_out.p, cur, c->qs.p, (int)nL, c->e_bits + c->mat_bits);
+                if (rc) return rc;
+                q = c->qs.p;
+                host_cnt[CNT_SORTS] += 1;
+            }
+            look_inv++;
+            EMC_TRY_CUDA(cudaEventRecord(c->ev[1], st));
+            k_lookup<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(q, (int32_t)nL, c->L, c->S, cf.fused, c->cnt.p);
+            EMC_CHECK_LAUNCH(c);
+            EMC_TRY_CUDA(cudaEventRecord(c->ev[2], st));
+            k_advance<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(q, (int32_t)nL, bp, c->L, c->G, c->S, lg, c->bins.p,
+                                                              c->qc.p, c->qx.p, c->ctl.p, c->cnt.p);
+            EMC_CHECK_LAUNCH(c);
+            k_crossing<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(c->qx.p, &c->ctl.p->nX, c->G, c->S, nxt, c->ctl.p);
+            EMC_CHECK_LAUNCH(c);
+            EMC_TRY_CUDA(cudaEventRecord(c->ev[3], st));
+            k_collision<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(c->qc.p, &c->ctl.p->nC, bp, c->L, c->G, c->src,
+                                                                c->S, lg, sv, c->bins.p, nxt, c->ctl.p, c->cnt.p);
+            EMC_CHECK_LAUNCH(c);
+            EMC_TRY_CUDA(cudaEventRecord(c->ev[4], st));
+            EMC_TRY_CUDA(cudaMemcpyAsync(c->ctl_host, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+            EMC_TRY_CUDA(cudaStreamSynchronize(st));
+            cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]); tm[3] += ms * 1e-3;
+            cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]); tm[0] += ms * 1e-3;
+            cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]); tm[1] += ms * 1e-3;
+            cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]); tm[2] += ms * 1e-3;
+            int64_t nC = c->ctl_host->nC;
+            host_cnt[CNT_EV_LOOKUP] += nL; host_cnt[CNT_EV_ADVANCE] += nL; host_cnt[CNT_EV_COLLISION] += nC;
+            host_cnt[CNT_INV_LOOKUP] += 1; host_cnt[CNT_INV_ADVANCE] += 1; host_cnt[CNT_INV_COLLISION] += nC > 0;
+            host_cnt[CNT_MAX_INFLIGHT] = std::max(host_cnt[CNT_MAX_INFLIGHT], nL);
+            nL = c->ctl_host->nL2;
+            std::swap(cur, nxt);
+            iterations++;
+        }
+    }
+
+    // gather results
+    unsigned long long dcnt[EMC_N_COUNTERS];
+    EMC_TRY_CUDA(cudaMemcpyAsync(dcnt, c->cnt.p, sizeof(dcnt), cudaMemcpyDeviceToHost, st));
+    EMC_TRY_CUDA(cudaMemcpyAsync(c->ctl_host, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    EMC_TRY_CUDA(cudaStreamSynchronize(st));
+    const Ctl& h = *c->ctl_host;
+    for (int k = 0; k < EMC_N_COUNTERS; ++k) res->counters[k] = (int64_t)dcnt[k] + host_cnt[k];
+    if (cf.history) {
+        res->counters[CNT_INV_LOOKUP] = res->counters[CNT_EV_LOOKUP];
+        res->counters[CNT_INV_ADVANCE] = res->counters[CNT_EV_ADVANCE];
+        res->counters[CNT_INV_COLLISION] = res->counters[CNT_EV_COLLISION];
+    }
+    res->counters[CNT_LOG_N] = (int64_t)h.log_n;
+    res->counters[CNT_SITE_N] = (int64_t)h.site_n;
+    res->counters[CNT_OVF] = h.ovf;
+    res->counters[CNT_ERR] = h.err;
+    res->counters[CNT_ERR_AUX] = h.err_aux;
+    for (int k = 0; k < 4; ++k) res->timings[k] = tm[k];
+    res->n_sites = (int64_t)h.site_n;
+    res->n_logs = (int64_t)h.log_n;
+    res->iterations = iterations;
+    res->error = h.err;
+    res->error_gid = h.err_aux;
+    return 0;
+}
+
+extern "C" int emc_run_batch(emc_ctx* c, const emc_batch_args* a, emc_batch_result* res)
+{
+    if (!c || !a || !res) return fail_arg("emc_run_batch: null argument");
+    if (!c->configured) return fail_arg("emc_configure first");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    std::memset(res, 0, sizeof(*res));
+    int64_t l0 = c->launches;
+    int reruns = 0;
+    for (;;) {
+        int rc = run_batch_once(c, a, res);
+        if (rc) return rc;
+        if (res->error) break;
+        int ovf = (int)res->counters[CNT_OVF];
+        if (ovf == 0) break;
+        // grow-and-rerun (R:107-111, R:122-142): a batch is a pure function of
+        // its inputs, so the rerun reproduces the same physics
+        size_t need;
+        if (ovf == 2) {
+            need = std::max<size_t>(2 * c->sites.parent.n, (size_t)res->n_sites + 1024);
+            c->sites.release(); c->banks[1 - c->cur_bank].release();
+            c->bkey_in.release(); c->bkey_out.release(); c->bidx_in.release(); c->bidx_out.release();
+            if ((rc = alloc_sites(c, need))) return rc;
+        } else {
+            need = std::max<size_t>(2 * c->lg_gid.n, (size_t)res->n_logs + 1024);
+            c->lg_gid.release(); c->lg_ord.release(); c->lg_bin.release(); c->lg_val.release();
+            c->lkey_in.release(); c->lkey_out.release(); c->lval_out.release();
+            if ((rc = alloc_logs(c, need))) return rc;
+        }
+        reruns++;
+    }
+    res->reruns = reruns;
+    if (res->error) { res->launches = c->launches - l0; return 0; }
+
+    // canonical bank: sort this rank's sites by (parent, ordinal)  (R:221-228)
+    cudaStream_t st = c->stream;
+    int64_t n = res->n_sites;
+    if (n > 0) {
+        DSites sv = c->sites.view();
+        k_bank_keys<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(sv.parent, sv.ord, n, c->cfg.gid_lo, c->bkey_in.p,
+                                                               c->bidx_in.p);
+        EMC_CHECK_LAUNCH(c);
+        int kb = bits_for(c->cfg.n_assigned) + 20;
+        int rc = sort_cub64(c, c->bkey_in.p, c->bkey_out.p, c->bidx_in.p, c->bidx_out.p, n, kb);
+        if (rc) return rc;
+        SiteBufs& out = c->banks[1 - c->cur_bank];
+        if (out.parent.n < (size_t)n && out.alloc(std::max<size_t>(n, c->sites.parent.n))) return EMC_E_OOM;
+        k_bank_gather<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(c->bidx_out.p, n, sv, out.view());
+        EMC_CHECK_LAUNCH(c);
+    }
+    c->cur_bank = 1 - c->cur_bank;
+    c->bank_n = n;
+    // deterministic mode: sort the log by (bin, gid, ordinal) now
+    c->log_n = res->n_logs;
+    if (c->cfg.use_logs && c->log_n > 0) {
+        k_log_keys<<<grid_for(c->log_n, 256, 1 << 30), 256, 0, st>>>(c->lg_gid.p, c->lg_ord.p, c->lg_bin.p,
+                                                                     c->log_n, c->cfg.gid_lo, c->gid_bits,
+                                                                     c->lkey_in.p);
+        EMC_CHECK_LAUNCH(c);
+        int bb = bits_for(c->n_bins);
+        int rc = sort_cub64(c, c->lkey_in.p, c->lkey_out.p, c->lg_val.p, c->lval_out.p, c->log_n,
+                            bb + c->gid_bits + 17);
+        if (rc) return rc;
+    }
+    EMC_TRY_CUDA(cudaStreamSynchronize(st));
+    res->launches = c->launches - l0;
+    return 0;
+}
+
+extern "C" int emc_reduce_bins(emc_ctx* c, const double* init, double* out, int64_t n_bins)
+{
+    if (!c || !out || n_bins != c->n_bins) return fail_arg("emc_reduce_bins: bad arguments");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    if (init) EMC_TRY_CUDA(cudaMemcpyAsync(c->bins_init.p, init, n_bins * 8, cudaMemcpyHostToDevice, st));
+    else EMC_TRY_CUDA(cudaMemsetAsync(c->bins_init.p, 0, n_bins * 8, st));
+    if (c->cfg.use_logs) {
+        k_log_fold<<<grid_for(n_bins, 128, 1 << 30), 128, 0, st>>>(c->lkey_out.p, c->lval_out.p, c->log_n,
+                                                                    c->gid_bits + 17, (int32_t)n_bins,
+                                                                    c->bins_init.p, c->bins_out.p);
+        EMC_CHECK_LAUNCH(c);
+        EMC_TRY_CUDA(cudaMemcpyAsync(out, c->bins_out.p, n_bins * 8, cudaMemcpyDeviceToHost, st));
+        EMC_TRY_CUDA(cudaStreamSynchronize(st));
+    } else {
+        std::vector<double> b(n_bins);
+        EMC_TRY_CUDA(cudaMemcpyAsync(b.data(), c->bins.p, n_bins * 8, cudaMemcpyDeviceToHost, st));
+        EMC_TRY_CUDA(cudaStreamSynchronize(st));
+        for (int64_t k = 0; k < n_bins; ++k) out[k] = (init ? init[k] : 0.0) + b[k];
+    }
+    return 0;
+}
+
+extern "C" int emc_bank_size(emc_ctx* c, int64_t* n)
+{
+    if (!c || !n) return fail_arg("null");
+    *n = c->bank_n;
+    return 0;
+}
+
+extern "C" int emc_bank_device(emc_ctx* c, void* ptrs[9])
+{
+    if (!c || !ptrs) return fail_arg("null");
+    SiteBufs& b = c->bank();
+    void* p[9] = {b.parent.p, b.ord.p, b.x.p, b.y.p, b.z.p, b.dx.p, b.dy.p, b.dz.p, b.E.p};
+    for (int k = 0; k < 9; ++k) ptrs[k] = p[k];
+    return 0;
+}
+
+extern "C" int emc_bank_copy(emc_ctx* c, int64_t start, int64_t n, int64_t* parent, int32_t* ord, double* x,
+                             double* y, double* z, double* dx, double* dy, double* dz, double* E)
+{
+    if (!c || start < 0 || n < 0 || start + n > c->bank_n) return fail_arg("emc_bank_copy: range");
+    if (n == 0) return 0;
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    SiteBufs& b = c->bank();
+    EMC_TRY_CUDA(cudaMemcpyAsync(parent, b.parent.p + start, n * 8, cudaMemcpyDeviceToHost, st));
+    EMC_TRY_CUDA(cudaMemcpyAsync(ord, b.ord.p + start, n * 4, cudaMemcpyDeviceToHost, st));
+    double* dst[7] = {x, y, z, dx, dy, dz, E};
+    double* srcs[7] = {b.x.p, b.y.p, b.z.p, b.dx.p, b.dy.p, b.dz.p, b.E.p};
+    for (int k = 0; k < 7; ++k)
+        EMC_TRY_CUDA(cudaMemcpyAsync(dst[k], srcs[k] + start, n * 8, cudaMemcpyDeviceToHost, st));
+    EMC_TRY_CUDA(cudaStreamSynchronize(st));
+    return 0;
+}
+
+// ------------------------------------------------------------- API ops ---
+
+namespace {
+template <class T>
+int to_dev(DBuf<T>& b, const T* h, int64_t n, cudaStream_t st)
+{
+    if (b.alloc(std::max<int64_t>(n, 1))) return EMC_E_OOM;
+    if (n) EMC_TRY_CUDA(cudaMemcpyAsync(b.p, h, n * sizeof(T), cudaMemcpyHostToDevice, st));
+    return 0;
+}
+template <class T>
+int to_host(T* h, const DBuf<T>& b, int64_t n, cudaStream_t st)
+{
+    if (n) EMC_TRY_CUDA(cudaMemcpyAsync(h, b.p, n * sizeof(T), cudaMemcpyDeviceToHost, st));
+    return 0;
+}
+}  // namespace
+
+extern "C" int emc_xs_lookup(emc_ctx* c, int64_t n, const int32_t* mats, const double* E, double* sums,
+                             double* partials, int32_t max_comp)
+{
+    if (!c || !c->have_lib) return fail_arg("upload a library first");
+    if (n < 0 || (partials && max_comp < c->max_comp)) return fail_arg("emc_xs_lookup: bad arguments");
+    for (int64_t i = 0; i < n; ++i)
+        if (mats[i] < 0 || mats[i] >= c->n_materials) return fail_arg("unknown material");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DBuf<int32_t> dm; DBuf<double> de, ds, dp;
+    int rc = to_dev(dm, mats, n, st) | to_dev(de, E, n, st);
+    if (rc || ds.alloc(std::max<int64_t>(1, n * 5))) return EMC_E_OOM;
+    if (partials && dp.alloc(std::max<int64_t>(1, n * max_comp * 4))) return EMC_E_OOM;
+    if (partials) EMC_TRY_CUDA(cudaMemsetAsync(dp.p, 0, n * max_comp * 4 * 8, st));
+    if (n) {
+        k_api_macro<<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(c->L, n, dm.p, de.p, max_comp, ds.p,
+                                                                 partials ? dp.p : nullptr);
+        EMC_CHECK_LAUNCH(c);
+    }
+    to_host(sums, ds, n * 5, st);
+    if (partials) to_host(partials, dp, n * max_comp * 4, st);
+    EMC_TRY_CUDA(cudaStreamSynchronize(st));
+    dm.release(); de.release(); ds.release(); dp.release();
+    return 0;
+}
+
+extern "C" int emc_locate(emc_ctx* c, int64_t n, const double* pos, int32_t* out)
+{
+    if (!c || !c->have_geom) return fail_arg("upload a geometry first");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DBuf<double> dp; DBuf<int32_t> dout;
+    if (to_dev(dp, pos, 3 * n, st) || dout.alloc(std::max<int64_t>(1, 3 * n))) return EMC_E_OOM;
+    if (n) { k_api_locate<<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(c->G, n, dp.p, dout.p); EMC_CHECK_LAUNCH(c); }
+    to_host(out, dout, 3 * n, st);
+    EMC_TRY_CUDA(cudaStreamSynchronize(st));
+    dp.release(); dout.release();
+    return 0;
+}
+
+extern "C" int emc_distance(emc_ctx* c, int64_t n, const double* pos, const double* dir, const int32_t* cell,
+                            double* dist, int32_t* surf)
+{
+    if (!c || !c->have_geom) return fail_arg("upload a geometry first");
+    for (int64_t i = 0; i < n; ++i)
+        if (cell[2 * i] == KIND_FUEL && (cell[2 * i + 1] < 0 || cell[2 * i + 1] >= c->G.n_axial))
+            return fail_arg("fuel cell axial index out of range");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DBuf<double> dp, dd, ddist; DBuf<int32_t> dc, ds;
+    if (to_dev(dp, pos, 3 * n, st) || to_dev(dd, dir, 3 * n, st) || to_dev(dc, cell, 2 * n, st) ||
+        ddist.alloc(std::max<int64_t>(1, n)) || ds.alloc(std::max<int64_t>(1, n)))
+        return EMC_E_OOM;
+    if (n) {
+        k_api_distance<<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(c->G, n, dp.p, dd.p, dc.p, ddist.p, ds.p);
+        EMC_CHECK_LAUNCH(c);
+    }
+    to_host(dist, ddist, n, st); to_host(surf, ds, n, st);
+    EMC_TRY_CUDA(cudaStreamSynchronize(st));
+    dp.release(); dd.release(); ddist.release(); dc.release(); ds.release();
+    return 0;
+}
+
+extern "C" int emc_particle_ops(emc_ctx* c, int64_t n, const uint64_t* states, const double* sigma_t, double* iso,
+                                double* dcol, uint64_t* st_iso, uint64_t* st_dcol)
+{
+    if (!c) return fail_arg("null ctx");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DBuf<uint64_t> ds, d1, d2; DBuf<double> dsig, diso, dcl;
+    if (to_dev(ds, states, n, st) || to_dev(dsig, sigma_t, n, st) || diso.alloc(std::max<int64_t>(1, 3 * n)) ||
+        dcl.alloc(std::max<int64_t>(1, n)) || d1.alloc(std::max<int64_t>(1, n)) || d2.alloc(std::max<int64_t>(1, n)))
+        return EMC_E_OOM;
+    if (n) {
+        k_api_particle_ops<<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(n, ds.p, dsig.p, diso.p, dcl.p, d1.p, d2.p);
+        EMC_CHECK_LAUNCH(c);
+    }
+    to_host(iso, diso, 3 * n, st); to_host(dcol, dcl, n, st); to_host(st_iso, d1, n, st); to_host(st_dcol, d2, n, st);
+    EMC_TRY_CUDA(cudaStreamSynchronize(st));
+    ds.release(); d1.release(); d2.release(); dsig.release(); diso.release(); dcl.release();
+    return 0;
+}
+
+namespace {
+__global__ void k_qkeys_energy(const int32_t* q, int64_t n, const double* E, uint64_t* keys)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint64_t b = (uint64_t)__double_as_longlong(E[q[i]]);
+    keys[i] = (b >> 63) ? ~b : (b | 0x8000000000000000ULL);   // total order of doubles
+}
+__global__ void k_qkeys_mat(const int32_t* q, int64_t n, const int32_t* mat, uint32_t* keys)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    keys[i] = (uint32_t)mat[q[i]] ^ 0x80000000u;
+}
+}  // namespace
+
+extern "C" int emc_sort_queue(emc_ctx* c, int64_t n, const int32_t* q, int64_t n_slots, const int32_t* mat,
+                              const double* E, int32_t* out)
+{
+    if (!c || n < 0) return fail_arg("emc_sort_queue: bad arguments");
+    for (int64_t i = 0; i < n; ++i) if (q[i] < 0 || q[i] >= n_slots) return fail_arg("queue entry out of range");
+    if (n < 2) { if (n == 1) out[0] = q[0]; return 0; }
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DBuf<int32_t> dq, dq2, dm; DBuf<double> de; DBuf<uint64_t> k1, k2; DBuf<uint32_t> m1, m2;
+    if (to_dev(dq, q, n, st) || to_dev(dm, mat, n_slots, st) || to_dev(de, E, n_slots, st) || dq2.alloc(n) ||
+        k1.alloc(n) || k2.alloc(n) || m1.alloc(n) || m2.alloc(n))
+        return EMC_E_OOM;
+    // two stable passes == the reference's argsort(E) then argsort(mat) (K:1026-1033)
+    k_qkeys_energy<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(dq.p, n, de.p, k1.p);
+    EMC_CHECK_LAUNCH(c);
+    int rc = sort_cub64(c, k1.p, k2.p, dq.p, dq2.p, n, 64);
+    if (rc) return rc;
+    k_qkeys_mat<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(dq2.p, n, dm.p, m1.p);
+    EMC_CHECK_LAUNCH(c);
+    rc = sort_cub64(c, m1.p, m2.p, dq2.p, dq.p, n, 32);
+    if (rc) return rc;
+    to_host(out, dq, n, st);
+    EMC_TRY_CUDA(cudaStreamSynchronize(st));
+    dq.release(); dq2.release(); dm.release(); de.release(); k1.release(); k2.release(); m1.release(); m2.release();
+    return 0;
+}
+
+extern "C" int emc_replay_bins(emc_ctx* c, int64_t n, const int32_t* bin, const double* val, int32_t n_bins,
+                               double* sums)
+{
+    if (!c || n < 0 || n_bins < 1) return fail_arg("emc_replay_bins: bad arguments");
+    for (int64_t i = 0; i < n; ++i) if (bin[i] < 0 || bin[i] >= n_bins) return fail_arg("bin out of range");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    int pb = bits_for(n), bb = bits_for(n_bins);
+    if (pb + bb > 64) { g_err = "replay too large"; return EMC_E_RANGE; }
+    DBuf<int32_t> db; DBuf<double> dv, dv2, dinit, dout; DBuf<uint64_t> k1, k2;
+    if (to_dev(db, bin, n, st) || to_dev(dv, val, n, st) || dv2.alloc(std::max<int64_t>(n, 1)) ||
+        k1.alloc(std::max<int64_t>(n, 1)) || k2.alloc(std::max<int64_t>(n, 1)) || dinit.alloc(n_bins) ||
+        dout.alloc(n_bins))
+        return EMC_E_OOM;
+    EMC_TRY_CUDA(cudaMemsetAsync(dinit.p, 0, n_bins * 8, st));
+    if (n) {
+        k_replay_keys<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(db.p, n, pb, k1.p);
+        EMC_CHECK_LAUNCH(c);
+        int rc = sort_cub64(c, k1.p, k2.p, dv.p, dv2.p, n, pb + bb);
+        if (rc) return rc;
+    }
+    k_log_fold<<<grid_for(n_bins, 128, 1 << 30), 128, 0, st>>>(k2.p, dv2.p, n, pb, n_bins, dinit.p, dout.p);
+    EMC_CHECK_LAUNCH(c);
+    to_host(sums, dout, n_bins, st);
+    EMC_TRY_CUDA(cudaStreamSynchronize(st));
+    db.release(); dv.release(); dv2.release(); k1.release(); k2.release(); dinit.release(); dout.release();
+    return 0;
+}
+
+extern "C" int emc_lcg_skip(emc_ctx* c, int64_t n, const uint64_t* s, const uint64_t* k, uint64_t* out)
+{
+    if (!c) return fail_arg("null ctx");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DBuf<uint64_t> ds, dk, dout;
+    if (to_dev(ds, s, n, st) || to_dev(dk, k, n, st) || dout.alloc(std::max<int64_t>(n, 1))) return EMC_E_OOM;
+    if (n) { k_api_lcg_skip<<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(n, ds.p, dk.p, dout.p); EMC_CHECK_LAUNCH(c); }
+    to_host(out, dout, n, st);
+    EMC_TRY_CUDA(cudaStreamSynchronize(st));
+    ds.release(); dk.release(); dout.release();
+    return 0;
+}
+
+extern "C" int emc_libm_eval(emc_ctx* c, int64_t n, const double* x, double* out)
+{
+    if (!c) return fail_arg("null ctx");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DBuf<double> dx, dout;
+    if (to_dev(dx, x, n, st) || dout.alloc(std::max<int64_t>(3 * n, 1))) return EMC_E_OOM;
+    if (n) { k_api_libm<<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(n, dx.p, dout.p); EMC_CHECK_LAUNCH(c); }
+    to_host(out, dout, 3 * n, st);
+    EMC_TRY_CUDA(cudaStreamSynchronize(st));
+    dx.release(); dout.release();
+    return 0;
+}

@@ -1,0 +1,262 @@
+"""Batch coordinator: the drop-in ``run_replicated`` (eventmc/replication.py,
+R:<line>) over the GPU engine, plus the weak-scaling harness.
+
+Per batch (R:198-286): run this rank's particle block on its GPU
+(emc_run_batch: source, event loop, canonical bank sort), map device error
+codes to exceptions (R:214-219), gather the bank and reduce tallies across
+ranks (distributed.py), compute k (R:243-249), check neutron bookkeeping
+(R:250-257), accumulate counters (R:259-269) and resample the next source
+from the global canonical bank (R:271-280).  In a single process the GPU is
+the whole worker pool: ``config.workers`` is validated but all particles run
+on device 0; under torch.distributed each rank drives its own GPU.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+from . import prng, xslib
+from .distributed import (BANK_DTYPES, World, allgather_array, block_of, chained_fold,
+                          combine_counters, current_world, device_view, fast_bins, gather_bank)
+from .engine import DeviceEngine
+from .errors import (ConfigurationError, EventMCError, GeometryError, PhysicsError,
+                     PopulationCollapseError, RunawayHistoryError, StreamOverlapError)
+from .tally import KeffSeries, TallyLayout, batch_statistics
+from .transport import FissionBank, RunConfig, RunResult
+
+# device error code -> (exception, message)   (R:28-38)
+_ERRORS = {
+    1: (GeometryError, "no boundary intersection"),
+    2: (GeometryError, "particle outside the cell box"),
+    3: (StreamOverlapError, "history consumed a full RNG stride"),
+    4: (RunawayHistoryError, "history exceeded the contribution-log cap"),
+    5: (EventMCError, "event queue invariant violated"),
+    6: (PhysicsError, "sigma_t <= 0 (void materials unsupported)"),
+}
+# counter indices: kernels.py:81-103
+_COUNTER_SUMS = (("captures", 5), ("fissions", 6), ("sourced", 7), ("energy_clamps", 9),
+                 ("interp_transport", 10), ("interp_score", 11), ("events_lookup", 12),
+                 ("events_advance", 13), ("events_collision", 14), ("invocations_lookup", 15),
+                 ("invocations_advance", 16), ("invocations_collision", 17), ("sorts", 18))
+_COUNTER_MAXES = (("max_draws_per_history", 8), ("max_log_entries_per_history", 20),
+                  ("max_in_flight_observed", 19))
+
+_ENGINES: dict[int, DeviceEngine] = {}
+
+
+def engine_for(device: int, library, pincell) -> DeviceEngine:
+    """Per-device engine reused across runs; re-uploads changed inputs only."""
+    eng = _ENGINES.get(device)
+    if eng is None:
+        eng = _ENGINES[device] = DeviceEngine(device)
+    if eng.library_obj is None or eng.library_obj() is not library:
+        eng.upload_library(library)
+    if eng.pincell_obj is None or eng.pincell_obj() is not pincell:
+        eng.upload_geometry(pincell)
+    return eng
+
+
+def _local_device(world: World) -> int:
+    if not world.distributed:
+        return 0
+    import torch
+    return torch.cuda.current_device() if world.device_backend else 0
+
+
+def run_replicated(config: RunConfig, library, pincell, index=None, *,
+                   on_batch=None) -> RunResult:
+    """Run the configured k-eigenvalue problem on this process's GPU(s).
+
+    ``on_batch(b, phase, engine)`` (phase 'start'/'end') is an optional
+    instrumentation hook (bench.py records CUDA events through it)."""
+    config.validate()
+    ppb = config.particles_per_batch
+    for mid in list(pincell.fuel_material_ids) + [pincell.moderator_material_id]:
+        if mid < 0 or mid >= library.n_materials:
+            raise ConfigurationError(f"geometry references material {mid} "
+                                     f"but the library has {library.n_materials}")
+    if config.accel != "binary" and index is not None and config.accel == "unionized" \
+            and index.merged_channels is None:
+        xslib.merge_channels(library, index)   # API parity (R:145-152); device search is log-hashed
+
+    world = current_world()
+    if world.distributed and world.size > ppb:
+        raise ConfigurationError("more ranks than particles per batch")
+    g_lo, g_hi = block_of(world.rank, world.size, ppb)
+    eng = engine_for(_local_device(world), library, pincell)
+    eng.configure(config, g_lo, g_hi - g_lo)
+
+    layout = TallyLayout(pincell.n_axial)
+    use_logs = config.reduction == "deterministic"
+    weight = float(ppb)
+    n_batches = config.n_batches
+    batch_sums = np.zeros((n_batches, layout.n_bins))
+    keff_values = np.zeros(n_batches)
+    run_counters: dict[str, int] = {}
+    timings = {"lookup": 0.0, "advance": 0.0, "collision": 0.0, "sort": 0.0,
+               "reduce": 0.0, "merge": 0.0}
+    inactive_wall = active_wall = 0.0
+    k_run = 1.0
+    last_bank_cols = None
+    launches = 0
+    nuclide_lookups_active = 0
+    act = dict(lookup_active_s=0.0, lookup_launches_active=0, h2d_bytes_active=0,
+               d2h_bytes_active=0)
+
+    for b in range(n_batches):
+        active = b >= config.inactive_batches
+        if on_batch is not None:
+            on_batch(b, "start", eng)
+        t_batch = time.perf_counter()
+        out = eng.run_batch(b, k_run, batch0=(b == 0), score=active)
+        launches += out.launches
+        errs = allgather_array(world, np.array([out.error, out.error_gid], np.int64))
+        for code, gid in errs:
+            if code:
+                cls, msg = _ERRORS[int(code)]
+                raise cls(f"{msg} (batch {b}, particle {int(gid)})")
+
+        # fission bank: global canonical order = rank-ordered concatenation
+        t0 = time.perf_counter()
+        counts = allgather_array(world, np.array([out.n_sites], np.int64))[:, 0]
+        n_bank = int(counts.sum())
+        global_cols = None
+        if world.distributed:
+            local = [device_view(p, max(out.n_sites, 1), dt, eng.device)
+                     for p, dt in zip(eng.bank_device_ptrs(), BANK_DTYPES)] \
+                if world.device_backend else \
+                [__import__("torch").as_tensor(c) for c in eng.bank_to_host()]
+            global_cols = gather_bank(world, local, counts)
+        timings["merge"] += time.perf_counter() - t0
+
+        # tallies + k
+        t0 = time.perf_counter()
+        if use_logs:
+            sums = chained_fold(world, lambda init: eng.reduce_bins(init), layout.n_bins)
+        else:
+            sums = fast_bins(world, eng.reduce_bins(None))
+        timings["reduce"] += time.perf_counter() - t0
+        batch_sums[b] = sums
+        keff_values[b] = sums[layout.keff_bin] / weight
+
+        per_rank = allgather_array(world, out.counters)
+        sourced = int(per_rank[:, 7].sum())
+        deaths = int(per_rank[:, 5].sum() + per_rank[:, 6].sum())
+        if sourced != ppb or deaths != ppb:
+            raise EventMCError(f"neutron bookkeeping broken in batch {b}: {sourced} sourced, "
+                               f"{deaths} absorbed, {ppb} expected")
+        batch_counters = combine_counters(per_rank, _COUNTER_SUMS, _COUNTER_MAXES)
+        for name, _ in _COUNTER_SUMS:
+            run_counters[name] = run_counters.get(name, 0) + batch_counters[name]
+        for name, _ in _COUNTER_MAXES:
+            run_counters[name] = max(run_counters.get(name, 0), batch_counters[name])
+        if active:
+            nuclide_lookups_active += int(per_rank[:, 21].sum())
+            act["lookup_active_s"] += float(allgather_array(world, out.timings)[:, 0].sum())
+            act["lookup_launches_active"] += int(allgather_array(
+                world, np.array([out.iterations], np.int64)).sum())
+            # host<->device traffic of the batch: control block per iteration,
+            # counters + tally bins at the end (engine.py / emc_engine.cu)
+            act["h2d_bytes_active"] += 48 + 64
+            act["d2h_bytes_active"] += 48 * (out.iterations + 2) + 24 * 8 + layout.n_bins * 8
+        tim = allgather_array(world, out.timings).sum(axis=0)
+        for key, i in (("lookup", 0), ("advance", 1), ("collision", 2), ("sort", 3)):
+            timings[key] += float(tim[i])
+
+        # population control for the next batch (R:271-280)
+        if b < n_batches - 1:
+            if n_bank == 0:
+                raise PopulationCollapseError(f"no fission sites banked in batch {b}")
+            u, _ = prng.next_uniform(prng.batch_stream(config.seed, b))
+            if world.distributed:
+                src = global_cols[2:9]
+                eng.set_source_device([t.data_ptr() for t in src] if world.device_backend else
+                                      _host_to_device_bank(eng, src), n_bank, u, keep=src)
+            else:
+                eng.set_source_local(u)
+            k_run = keff_values[b]
+        else:
+            last_bank_cols = global_cols
+        wall = time.perf_counter() - t_batch
+        if on_batch is not None:
+            on_batch(b, "end", eng)
+        if active:
+            active_wall += wall
+        else:
+            inactive_wall += wall
+
+    # final canonical bank on the host
+    if world.distributed:
+        cols = [c.cpu().numpy() for c in last_bank_cols]
+    else:
+        cols = list(eng.bank_to_host())
+    bank = FissionBank(*cols)
+    act["d2h_bytes_active"] += 68 * len(bank)
+
+    keff = KeffSeries(keff_values, config.inactive_batches)
+    k_mean = k_stderr = tally_mean = tally_stderr = None
+    if config.active_batches >= 2:
+        k_mean, k_stderr = keff.statistics()
+        x = batch_sums[config.inactive_batches:, :layout.n_tally_bins] / weight
+        tally_mean, tally_stderr = batch_statistics(x)
+    inactive_rate = (config.inactive_batches * ppb / inactive_wall
+                     if config.inactive_batches > 0 and inactive_wall > 0.0 else None)
+    active_rate = (config.active_batches * ppb / active_wall
+                   if config.active_batches > 0 and active_wall > 0.0 else None)
+    timings["gpu_launches"] = launches
+    timings["nuclide_lookups_active"] = nuclide_lookups_active
+    timings.update(act)
+    return RunResult(keff=keff, k_mean=k_mean, k_stderr=k_stderr, tally_mean=tally_mean,
+                     tally_stderr=tally_stderr, batch_sums=batch_sums, layout=layout, bank=bank,
+                     timings=timings, inactive_wall=inactive_wall, active_wall=active_wall,
+                     inactive_rate=inactive_rate, active_rate=active_rate,
+                     counters=run_counters, config=config.echo(),
+                     library_fingerprint=xslib.library_fingerprint(library),
+                     geometry_fingerprint=pincell.fingerprint())
+
+
+def _host_to_device_bank(eng, cols):   # pragma: no cover - gloo + GPU mix is not a product path
+    raise ConfigurationError("multi-rank transport needs the NCCL backend (one GPU per rank)")
+
+
+@dataclass
+class ScalingRow:
+    workers: int
+    particles_per_worker: int
+    inactive_rate: float
+    active_rate: float
+    efficiency: float
+
+
+def weak_scaling_study(base_config: RunConfig, library, pincell, worker_list: list[int],
+                       particles_per_worker: int, index=None) -> list[ScalingRow]:
+    """particles_per_batch = W * particles_per_worker; efficiency =
+    active_rate(W) / (W * active_rate(1)) (R:329-355)."""
+    if not worker_list or worker_list[0] != 1 or sorted(worker_list) != list(worker_list):
+        raise ConfigurationError("worker list must be ascending and start at 1")
+    if base_config.active_batches < 1 or base_config.inactive_batches < 1:
+        raise ConfigurationError("scaling study needs at least one batch in each phase")
+    rows: list[ScalingRow] = []
+    base_rate = None
+    for w in worker_list:
+        cfg = replace(base_config, workers=w, particles_per_batch=w * particles_per_worker)
+        res = run_replicated(cfg, library, pincell, index=index)
+        if base_rate is None:
+            base_rate = res.active_rate
+        rows.append(ScalingRow(w, particles_per_worker, res.inactive_rate, res.active_rate,
+                               res.active_rate / (w * base_rate)))
+    return rows
+
+
+def warm_up() -> None:
+    """Create the device context and run a miniature problem (loads the
+    kernels so later timings exclude module load)."""
+    from .presets import analytic_infinite_medium
+    library, pincell = analytic_infinite_medium()
+    for mode in ("history", "event"):
+        cfg = RunConfig(particles_per_batch=8, inactive_batches=1, active_batches=2,
+                        mode=mode, max_in_flight=4, accel="unionized")
+        run_replicated(cfg, library, pincell)

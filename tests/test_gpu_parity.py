@@ -1,0 +1,192 @@
+"""GPU parity: libemc against the reference's golden outputs (bit-exact)
+and against the C oracle on the same inputs.
+
+Golden data come from running the reference itself (tests/golden/make_golden.py);
+the oracle (oracle/) is the checker for inputs the goldens do not cover.
+"""
+
+import os
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, golden_geom, golden_lib_arrays, golden_library
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2403_12345_b200")
+
+
+def _cell(pm):
+    return P.Pincell(n_axial=pm["n_axial"], fuel_material_ids=pm["fuel_material_ids"],
+                     moderator_material_id=pm["moderator_material_id"])
+
+
+def _config(run):
+    return P.RunConfig(**run["config"])
+
+
+RUNS = ["small_history", "small_event_cap16", "small_event_naive", "small_perturb17",
+        "small_seed6", "small_inact0", "small_hotsrc", "analytic_event_w2", "c1_event"]
+
+
+@pytest.mark.parametrize("name", RUNS)
+def test_run_matches_reference_fingerprint(golden, name):
+    run = golden["runs"][name]
+    pm = golden["problems"][run["problem"]]
+    lib = golden_library(run["problem"])
+    res = P.run_replicated(_config(run), lib, _cell(pm))
+    z = np.load(os.path.join(GOLDEN, f"run_{name}.npz"))
+    assert np.array_equal(res.keff.values, z["keff"]), "k series differs"
+    assert np.array_equal(res.batch_sums, z["batch_sums"]), "batch sums differ"
+    assert len(res.bank) == run["bank_len"]
+    assert res.physics_fingerprint() == run["fingerprint"]
+    for k in ("sourced", "captures", "fissions", "energy_clamps", "events_lookup",
+              "events_advance", "events_collision", "max_draws_per_history",
+              "interp_transport", "interp_score", "max_log_entries_per_history"):
+        assert res.counters[k] == run["counters"][k], k
+
+
+def test_fast_reduction_close(golden):
+    run = golden["runs"]["small_fast"]
+    pm = golden["problems"]["small"]
+    res = P.run_replicated(_config(run), golden_library("small"), _cell(pm))
+    z = np.load(os.path.join(GOLDEN, "run_small_fast.npz"))
+    # atomics reorder the sums: contract is 1e-10 relative (north star)
+    assert np.allclose(res.keff.values, z["keff"], rtol=1e-10, atol=0)
+
+
+def test_event_caps_sort_variants_equal(golden):
+    run = golden["runs"]["small_history"]
+    pm = golden["problems"]["small"]
+    lib = golden_library("small")
+    base = _config(run)
+    ref = run["fingerprint"]
+    for cap in (1, 16, 400):
+        for sort in (True, False):
+            cfg = replace(base, mode="event", max_in_flight=cap, sort_enabled=sort)
+            assert P.run_replicated(cfg, lib, _cell(pm)).physics_fingerprint() == ref, (cap, sort)
+    cfg = replace(base, mode="event", max_in_flight=64, accel="unionized", sort_every_n=3)
+    idx = P.build_unionized_index(lib, merged=True)
+    assert P.run_replicated(cfg, lib, _cell(pm), index=idx).physics_fingerprint() == ref
+
+
+def test_macro_lookup_matches_reference(golden):
+    z = np.load(os.path.join(GOLDEN, "lookup_small.npz"))
+    lib = golden_library("small")
+    sums, parts = P.xslib.macro_lookup_batch(lib, z["mats"], z["energies"])
+    assert np.array_equal(sums, z["sums"])
+    assert np.array_equal(parts, z["partials"][:, :parts.shape[1]])
+
+
+def test_geometry_matches_reference(golden):
+    z = np.load(os.path.join(GOLDEN, "geometry_c1.npz"))
+    cell = _cell(golden["problems"]["c1"])
+    loc = P.geometry.locate_batch(cell, z["pts"])
+    assert np.array_equal(loc[:, 0], z["kind"])
+    assert np.array_equal(loc[:, 1], z["axial"])
+    assert np.array_equal(loc[:, 2], z["mat"])
+    from paper_2403_12345_b200.engine import api_engine
+    inside = z["kind"] >= 0
+    cells = np.stack([z["kind"], z["axial"]], 1).astype(np.int32)[inside]
+    dist, surf = api_engine(pincell=cell).distance(z["pts"][inside], z["dirs"][inside], cells)
+    assert np.array_equal(surf, z["surf"][inside])
+    assert np.array_equal(dist, z["dist"][inside])
+
+
+def test_particle_ops_match_reference():
+    z = np.load(os.path.join(GOLDEN, "particle_ops.npz"))
+    from paper_2403_12345_b200.engine import api_engine
+    iso, dcol, _, _ = api_engine().particle_ops(z["states"], np.full(z["states"].shape[0], 1.7))
+    assert np.array_equal(iso, z["iso"])
+    assert np.array_equal(dcol, z["dcol"])
+
+
+def test_device_libm_matches_glibc():
+    from paper_2403_12345_b200.engine import api_engine
+    rng = np.random.default_rng(7)
+    s = rng.integers(0, 2**63 - 1, 2_000_000, dtype=np.int64).astype(np.uint64)
+    u = s.astype(np.float64) * 2.0**-63
+    u[u >= 1.0] = 1.0 - 2.0**-53
+    x1 = 1.0 - u
+    x2 = 2.0 * np.pi * u
+    got1 = api_engine().libm(x1)
+    got2 = api_engine().libm(x2)
+    import math
+    # host glibc via math (libm log/sin/cos, not numpy SIMD)
+    for i in range(0, x1.shape[0], 97):
+        assert got1[i, 0] == math.log(x1[i])
+        assert got2[i, 1] == math.sin(x2[i])
+        assert got2[i, 2] == math.cos(x2[i])
+
+
+def test_lcg_skip_matches_host():
+    from paper_2403_12345_b200.engine import api_engine
+    rng = np.random.default_rng(3)
+    s = rng.integers(0, 2**62, 1000, dtype=np.int64).astype(np.uint64)
+    k = rng.integers(0, 2**40, 1000, dtype=np.int64).astype(np.uint64)
+    out = api_engine().lcg_skip(s, k)
+    for i in range(1000):
+        assert int(out[i]) == P.prng.skip_ahead(int(s[i]), int(k[i]))
+
+
+def test_sort_queue_stable_oracle():
+    rng = np.random.RandomState(20240811)
+    n = 10**4
+    mats = rng.randint(0, 7, n).astype(np.int32)
+    ens = rng.choice([0.5, 1.0, 2.0, 4.0], n)
+    q = rng.permutation(n).astype(np.int32)
+    expected = sorted(range(n), key=lambda i: (mats[q[i]], ens[q[i]], i))
+    assert np.array_equal(P.sort_lookup_queue(q, mats, ens), q[np.array(expected)])
+
+
+def test_reduce_batch_replay():
+    rng = np.random.RandomState(5)
+    n = 5000
+    gid = rng.randint(0, 50, n).astype(np.int64)
+    binidx = rng.randint(0, 13, n).astype(np.int32)
+    vals = rng.uniform(0.1, 2.0, n)
+    ordn = np.zeros(n, np.int32)
+    got = P.reduce_batch([(gid, ordn, binidx, vals)], 13)
+    perm = np.argsort(gid, kind="stable")
+    ref = np.zeros(13)
+    for b, v in zip(binidx[perm], vals[perm]):
+        ref[b] += v
+    assert np.array_equal(got, ref)
+
+
+def test_error_paths(golden):
+    errs = golden["errors"]
+
+    def uniform_medium(ss, sc, sf, nu):
+        grid = np.array([1.0e-5, 2.0e7])
+        nuc = P.NuclideXS(grid, np.full(2, ss + sc + sf), np.full(2, ss), np.full(2, sc),
+                          np.full(2, sf), nu)
+        return P.Library([nuc], [P.Material(0, [(0, 1.0)])])
+    cell = P.analytic_infinite_medium()[1]
+    with pytest.raises(getattr(P, errs["pure_scatter_history"])):
+        P.run_replicated(P.RunConfig(particles_per_batch=1, inactive_batches=1,
+                                     active_batches=0, mode="history", seed=1),
+                         uniform_medium(5.0, 1e-13, 1e-13, 0.0), cell)
+    with pytest.raises(getattr(P, errs["runaway_log"])):
+        P.run_replicated(P.RunConfig(particles_per_batch=1, inactive_batches=0,
+                                     active_batches=1, mode="history", seed=1),
+                         uniform_medium(5.0, 1e-13, 1e-13, 0.0), cell)
+    # same guards in event mode
+    with pytest.raises(P.StreamOverlapError):
+        P.run_replicated(P.RunConfig(particles_per_batch=1, inactive_batches=1,
+                                     active_batches=0, mode="event", seed=1),
+                         uniform_medium(5.0, 1e-13, 1e-13, 0.0), cell)
+
+
+def test_oracle_agrees_on_fresh_problem():
+    """An input not in the goldens: GPU vs the C oracle, bit-exact."""
+    from oracle import driver
+    lib, cell = P.depleted_pincell(20, 3, 300, 6, seed=9)
+    cfg = P.RunConfig(particles_per_batch=2000, inactive_batches=2, active_batches=3,
+                      mode="event", seed=77, max_in_flight=700)
+    res = P.run_replicated(cfg, lib, cell)
+    ores = driver.run(dict(cfg.__dict__), lib.arrays(), cell.as_tuple())
+    assert res.physics_fingerprint() == driver.fingerprint(ores)
+    assert res.counters["events_lookup"] == ores["counters"]["events_lookup"]
