@@ -14,7 +14,7 @@ import os
 from .errors import NativeUnavailableError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libemc.so")
+LIB_PATH = os.environ.get("EMC_LIBRARY") or os.path.join(HERE, "libemc.so")
 
 N_COUNTERS = 24
 N_TIMINGS = 4

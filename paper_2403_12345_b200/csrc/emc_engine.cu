@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -109,6 +110,8 @@ struct emc_ctx {
     // library
     bool have_lib = false;
     DBuf<Rec> rec; DBuf<double> ch_s, nu; DBuf<int32_t> mat_off; DBuf<Comp> comp; DBuf<int32_t> hash;
+    DBuf<int32_t> mat_group, grp_off; DBuf<NucRef> gnuc; DBuf<DD> ddT;
+    int32_t n_groups = 0;
     DLib L{};
     int32_t n_materials = 0, max_comp = 0;
     int64_t lib_bytes = 0;
@@ -122,12 +125,11 @@ struct emc_ctx {
     bool configured = false;
     emc_run_config cfg{};
     int64_t nslots = 0;
-    int32_t nck = 0, n_bins = 0, kbin = 0, e_bits = 20, mat_bits = 1;
+    int32_t nck = 0, n_bins = 0, kbin = 0, e_bits = 20, mat_bits = 1, grp_bits = 0;
+    bool mat_major = true;
 
     // particle slots
-    DBuf<double> px, py, pz, dx, dy, dz, en, cm_t, cm_c, cm_f, cm_nsf, ckpt;
-    DBuf<uint64_t> rng; DBuf<int32_t> draws, ordctr, histlog, axial, mat, surf; DBuf<int64_t> gid;
-    DBuf<int8_t> kind;
+    DBuf<PState> ps; DBuf<double> ckpt;
     DSlots S{};
 
     // queues + sort scratch
@@ -189,15 +191,14 @@ extern "C" void emc_destroy(emc_ctx* c)
     if (!c) return;
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
-    for (auto* b : {&c->px, &c->py, &c->pz, &c->dx, &c->dy, &c->dz, &c->en, &c->cm_t, &c->cm_c, &c->cm_f,
-                    &c->cm_nsf, &c->ckpt, &c->ch_s, &c->nu, &c->zplanes, &c->bins, &c->bins_init,
+    for (auto* b : {&c->ckpt, &c->ch_s, &c->nu, &c->zplanes, &c->bins, &c->bins_init,
                     &c->bins_out, &c->lg_val, &c->lval_out})
         b->release();
-    for (auto* b : {&c->draws, &c->ordctr, &c->histlog, &c->axial, &c->mat, &c->surf, &c->mat_off, &c->hash,
-                    &c->fuel_mats, &c->qa, &c->qb, &c->qs, &c->qc, &c->qx, &c->bidx_in, &c->bidx_out,
-                    &c->lg_ord, &c->lg_bin})
+    for (auto* b : {&c->mat_off, &c->hash, &c->fuel_mats, &c->qa, &c->qb, &c->qs, &c->qc, &c->qx,
+                    &c->bidx_in, &c->bidx_out, &c->lg_ord, &c->lg_bin})
         b->release();
-    c->rng.release(); c->gid.release(); c->kind.release(); c->rec.release(); c->comp.release();
+    c->ps.release(); c->rec.release(); c->comp.release();
+    c->mat_group.release(); c->grp_off.release(); c->gnuc.release(); c->ddT.release();
     c->keys_in.release(); c->keys_out.release(); c->cub_tmp.release();
     c->bkey_in.release(); c->bkey_out.release(); c->lkey_in.release(); c->lkey_out.release();
     c->lg_gid.release(); c->cnt.release(); c->ctl.release();
@@ -280,7 +281,33 @@ extern "C" int emc_upload_library(emc_ctx* c, const emc_library* lib)
         }
     }
 
+    // composition groups: identical nuclide lists -> one group (see DLib)
+    std::vector<int32_t> hgroup(nm), hgoff(1, 0);
+    std::vector<NucRef> hgnuc;
+    std::vector<std::vector<int32_t>> sigs;
+    for (int64_t m = 0; m < nm; ++m) {
+        std::vector<int32_t> sig(lib->mat_nuc + lib->mat_off[m], lib->mat_nuc + lib->mat_off[m + 1]);
+        int32_t g = -1;
+        for (size_t j = 0; j < sigs.size(); ++j) if (sigs[j] == sig) { g = (int32_t)j; break; }
+        if (g < 0) {
+            g = (int32_t)sigs.size();
+            sigs.push_back(sig);
+            for (int32_t nid : sig)
+                hgnuc.push_back(NucRef{(int32_t)lib->grid_off[nid], (int32_t)(lib->grid_off[nid + 1] - lib->grid_off[nid]),
+                                       (int32_t)(nid * nbins), nid});
+            hgoff.push_back((int32_t)hgnuc.size());
+        }
+        hgroup[m] = g;
+    }
+    if (hgnuc.empty()) hgnuc.push_back(NucRef{0, 1, 0, 0});
+    std::vector<DD> hdd((size_t)std::max(maxc, 1) * nm, DD{0.0, 0.0});
+    for (int64_t m = 0; m < nm; ++m)
+        for (int64_t k = lib->mat_off[m]; k < lib->mat_off[m + 1]; ++k)
+            hdd[(size_t)(k - lib->mat_off[m]) * nm + m] = DD{hcomp[k].den, hcomp[k].dn};
+
     int rc = 0;
+    rc |= c->mat_group.alloc(nm); rc |= c->grp_off.alloc(hgoff.size()); rc |= c->gnuc.alloc(hgnuc.size());
+    rc |= c->ddT.alloc(hdd.size());
     rc |= c->rec.alloc(np); rc |= c->ch_s.alloc(np); rc |= c->nu.alloc(nn); rc |= c->mat_off.alloc(nm + 1);
     rc |= c->comp.alloc(hcomp.size()); rc |= c->hash.alloc(hhash.size());
     if (rc) return EMC_E_OOM;
@@ -290,8 +317,13 @@ extern "C" int emc_upload_library(emc_ctx* c, const emc_library* lib)
     EMC_TRY_CUDA(cudaMemcpy(c->mat_off.p, hmo.data(), (nm + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
     EMC_TRY_CUDA(cudaMemcpy(c->comp.p, hcomp.data(), hcomp.size() * sizeof(Comp), cudaMemcpyHostToDevice));
     EMC_TRY_CUDA(cudaMemcpy(c->hash.p, hhash.data(), hhash.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    EMC_TRY_CUDA(cudaMemcpy(c->mat_group.p, hgroup.data(), nm * sizeof(int32_t), cudaMemcpyHostToDevice));
+    EMC_TRY_CUDA(cudaMemcpy(c->grp_off.p, hgoff.data(), hgoff.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    EMC_TRY_CUDA(cudaMemcpy(c->gnuc.p, hgnuc.data(), hgnuc.size() * sizeof(NucRef), cudaMemcpyHostToDevice));
+    EMC_TRY_CUDA(cudaMemcpy(c->ddT.p, hdd.data(), hdd.size() * sizeof(DD), cudaMemcpyHostToDevice));
+    c->n_groups = (int32_t)sigs.size();
     c->L = DLib{c->rec.p, c->ch_s.p, c->nu.p, c->mat_off.p, c->comp.p, c->hash.p, key_lo, (int32_t)nbins,
-                shift, lo, hi};
+                shift, lo, hi, c->mat_group.p, c->grp_off.p, c->gnuc.p, c->ddT.p, (int32_t)nm, 0};
     c->n_materials = (int32_t)nm;
     c->max_comp = maxc;
     c->lib_bytes = (int64_t)(np * (sizeof(Rec) + 8) + hcomp.size() * sizeof(Comp) + hhash.size() * 4);
@@ -345,35 +377,41 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
     c->nslots = nslots;
     c->nck = cfg->fused ? std::max(0, (c->max_comp - 1) / kCkptStride) : 0;
     int rc = 0;
-    for (auto* b : {&c->px, &c->py, &c->pz, &c->dx, &c->dy, &c->dz, &c->en, &c->cm_t, &c->cm_c, &c->cm_f, &c->cm_nsf})
-        rc |= b->alloc(nslots);
+    rc |= c->ps.alloc(nslots);
     rc |= c->ckpt.alloc(std::max<int64_t>(1, (int64_t)c->nck * nslots));
-    rc |= c->rng.alloc(nslots); rc |= c->gid.alloc(nslots); rc |= c->kind.alloc(nslots);
-    for (auto* b : {&c->draws, &c->ordctr, &c->histlog, &c->axial, &c->mat, &c->surf, &c->qa, &c->qb, &c->qs, &c->qc, &c->qx})
+    for (auto* b : {&c->qa, &c->qb, &c->qs, &c->qc, &c->qx})
         rc |= b->alloc(nslots);
     rc |= c->keys_in.alloc(nslots); rc |= c->keys_out.alloc(nslots);
     rc |= c->bins.alloc(c->n_bins); rc |= c->bins_init.alloc(c->n_bins); rc |= c->bins_out.alloc(c->n_bins);
     if (rc) return EMC_E_OOM;
-    c->S = DSlots{c->px.p, c->py.p, c->pz.p, c->dx.p, c->dy.p, c->dz.p, c->en.p, c->rng.p, c->draws.p,
-                  c->ordctr.p, c->histlog.p, c->axial.p, c->mat.p, c->surf.p, c->gid.p, c->kind.p,
-                  c->cm_t.p, c->cm_c.p, c->cm_f.p, c->cm_nsf.p, c->ckpt.p, nslots, c->nck};
+    c->S = DSlots{c->ps.p, c->ckpt.p, nslots, c->nck};
     // fission bank: reference starts at n_assigned*6+1024 (R:92); ~1 site per
     // source particle is typical, so start at 2x and grow on overflow.
     if ((rc = alloc_sites(c, (size_t)(cfg->n_assigned * 2 + 4096)))) return rc;
     if (cfg->use_logs) {
         if ((rc = alloc_logs(c, (size_t)(cfg->n_assigned * 64 + 4096)))) return rc;
     }
-    // sort key: material bits + energy bits in 32 bits
-    int mb = 1;
+    // lookup sort key (32 bits): composition group | log-energy | material.
+    // Energy-major inside a group: all fuel segments share one nuclide list,
+    // so neighbouring lanes read the same grid records (see DLib).
+    int gb = 0;
+    while ((1 << gb) < c->n_groups) ++gb;
+    int mb = 0;
     while ((1 << mb) < c->n_materials) ++mb;
+    mb = std::min(mb, 32 - gb - 16);
+    c->grp_bits = gb;
     c->mat_bits = mb;
-    c->e_bits = std::min(22, 32 - mb);
-    int gb = 1;
-    while (((int64_t)1 << gb) < cfg->n_assigned) ++gb;
-    c->gid_bits = gb;
+    c->e_bits = std::min(24, 32 - gb - mb);
+    // EMC_SORT_MODE=material: material-major key (mat, log E) instead
+    const char* sm = getenv("EMC_SORT_MODE");
+    c->mat_major = !(sm && std::string(sm) == "energy");
+    if (c->mat_major) { c->grp_bits = 0; c->mat_bits = mb; c->e_bits = std::min(24, 32 - mb); }
+    int gidb = 1;
+    while (((int64_t)1 << gidb) < cfg->n_assigned) ++gidb;
+    c->gid_bits = gidb;
     int bb = 1;
     while ((1 << bb) < c->n_bins) ++bb;
-    if (bb + gb + 17 > 64) { g_err = "deterministic log key exceeds 64 bits"; return EMC_E_RANGE; }
+    if (bb + gidb + 17 > 64) { g_err = "deterministic log key exceeds 64 bits"; return EMC_E_RANGE; }
     // CUB scratch, sized for the largest sort we run
     size_t t1 = 0, t2 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint32_t*)nullptr, (uint32_t*)nullptr, (int32_t*)nullptr,
@@ -499,10 +537,12 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             bool do_sort = cf.sort_enabled && nL > 1 && (look_inv % cf.sort_every) == 0;
             EMC_TRY_CUDA(cudaEventRecord(c->ev[0], st));
             if (do_sort) {
-                k_sort_keys<<<grid_for(nL, BLK, 1 << 30), BLK, 0, st>>>(cur, (int32_t)nL, c->mat.p, c->en.p,
-                                                                        c->keys_in.p, c->e_bits);
+                k_sort_keys<<<grid_for(nL, BLK, 1 << 30), BLK, 0, st>>>(cur, (int32_t)nL, c->ps.p, c->L,
+                                                                        c->keys_in.p, c->e_bits, c->mat_bits,
+                                                                        c->mat_major);
                 EMC_CHECK_LAUNCH(c);
-                int rc = sort_cub(c, c->keys_in.p, c->keys_out.p, cur, c->qs.p, (int)nL, c->e_bits + c->mat_bits);
+                int rc = sort_cub(c, c->keys_in.p, c->keys_out.p, cur, c->qs.p, (int)nL,
+                                  c->grp_bits + c->e_bits + c->mat_bits);
                 if (rc) return rc;
                 q = c->qs.p;
                 host_cnt[CNT_SORTS] += 1;

@@ -26,17 +26,19 @@ __global__ void __launch_bounds__(128) k_history(BatchP bp, DLib L, DGeom G, DSr
         int64_t g = bp.g_lo + (int64_t)idx;
         sourced += 1;
         if (!source_particle(s, g, bp, L, G, src, S, ctl, clamps)) break;
-        uint64_t rng = S.rng[s];
-        int32_t draws = S.draws[s], ordc = 0, hist = 0;
-        double x = S.px[s], y = S.py[s], z = S.pz[s];
-        double dx = S.dx[s], dy = S.dy[s], dz = S.dz[s], E = S.en[s];
-        int kd = S.kind[s];
-        int32_t ax = S.axial[s], m = S.mat[s];
+        const PState& p0 = S.ps[s];
+        uint64_t rng = p0.b.rng;
+        int32_t draws = p0.d.draws, ordc = 0, hist = 0;
+        double x = p0.a.x, y = p0.a.y, z = p0.a.z;
+        double dx = p0.b.dx, dy = p0.b.dy, dz = p0.b.dz, E = p0.a.E;
+        int kd = p0.d.kind;
+        int32_t ax = p0.d.axial, m = p0.d.mat;
+        double* ck = S.ckpt + (int64_t)s * S.nck;
         bool fail = false;
         for (;;) {
             // --- lookup (K:573-710)
             double st, sc, sf, snf;
-            macro_tcf(L, m, E, st, sc, sf, snf, bp.fused ? S.ckpt + s : nullptr, S.nslots, S.nck);
+            macro_tcf(L, m, E, st, sc, sf, snf, bp.fused ? ck : nullptr, S.nck);
             interp += 4ull * (unsigned long long)(L.mat_off[m + 1] - L.mat_off[m]);
             nuc_lookups += (unsigned long long)(L.mat_off[m + 1] - L.mat_off[m]);
             ev_l += 1;
@@ -58,7 +60,7 @@ __global__ void __launch_bounds__(128) k_history(BatchP bp, DLib L, DGeom G, DSr
                     v[3] = __dmul_rn(fl, sf); v[4] = __dmul_rn(fl, snf);
                 } else {
                     double st2, sc2, sf2, snf2;
-                    macro_tcf(L, m, E, st2, sc2, sf2, snf2, nullptr, 0, 0);
+                    macro_tcf_simple(L, m, E, st2, sc2, sf2, snf2, nullptr, 0);
                     interp_score += 3ull * (unsigned long long)(L.mat_off[m + 1] - L.mat_off[m]);
                     v[1] = __dmul_rn(fl, st2); v[2] = __dmul_rn(fl, __dadd_rn(sc2, sf2));
                     v[3] = __dmul_rn(fl, sf2); v[4] = __dmul_rn(fl, snf2);
@@ -118,7 +120,7 @@ __global__ void __launch_bounds__(128) k_history(BatchP bp, DLib L, DGeom G, DSr
                 double u1 = draw(rng, draws);
                 double tgt = __dmul_rn(u1, st);
                 double pt_sel;
-                int32_t ksel = select_nuclide(L, S, s, e0, e1, bin, E, tgt, bp.fused != 0, pt_sel, interp);
+                int32_t ksel = select_nuclide(L, ck, S.nck, e0, e1, bin, E, tgt, bp.fused != 0, pt_sel, interp);
                 const Comp cs = L.comp[ksel];
                 double s_s, s_c, s_f;
                 micro_scf(L, cs, bin, E, s_s, s_c, s_f);

@@ -1,5 +1,5 @@
-// Event kernels of the transport loop (one launch per queue sweep) and the
-// history-based kernel.  Reference: kernels.py (K:<line>), replication.py (R:).
+// Event kernels of the transport loop (one launch per queue sweep).
+// Reference: kernels.py (K:<line>), replication.py (R:).
 //
 // Queue structure per event iteration (host loop in emc_engine.cu):
 //   q_look --sort(mat, E)--> k_lookup --> k_advance --+--> q_col  --> k_collision --+
@@ -7,6 +7,8 @@
 //      +------------------------- q_next (scatter / crossed / refilled) -----------+
 // Every in-flight particle is in q_look at the start of an iteration; deaths
 // refill their slot from the batch cursor inside k_collision (K:1191-1202).
+// Particle state is one 128-byte PState line per slot; kernels move whole
+// 32-byte sectors (P0..P3) with vector loads/stores.
 #pragma once
 #include "emc_device.cuh"
 
@@ -43,8 +45,9 @@ __device__ __forceinline__ bool source_particle(int32_t slot, int64_t g, const B
     uint64_t s = lcg_skip(bp.seed, off);
     if (g == bp.perturb_gid) s ^= 1ULL;
     int32_t draws = 0;
-    double x, y, z, dx, dy, dz, E;
+    P0 a; P1 b;
     if (bp.batch0) {
+        double x, y;
         for (;;) {
             double u1 = draw(s, draws), u2 = draw(s, draws);
             x = __dmul_rn(__dsub_rn(__dmul_rn(2.0, u1), 1.0), G.radius);
@@ -52,23 +55,25 @@ __device__ __forceinline__ bool source_particle(int32_t slot, int64_t g, const B
             if (__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)) < G.r2) break;
             if (draws >= kStride) { set_error(ctl, nullptr, ERR_STREAM_OVERLAP, g); return false; }
         }
-        z = __dmul_rn(draw(s, draws), G.height);
+        a.x = x; a.y = y;
+        a.z = __dmul_rn(draw(s, draws), G.height);
         double ua = draw(s, draws), ub = draw(s, draws);
-        isotropic(ua, ub, dx, dy, dz);
+        isotropic(ua, ub, b.dx, b.dy, b.dz);
         double ue = draw(s, draws);
-        E = clamp_energy(__dmul_rn(-bp.fission_t, emc_log(__dsub_rn(1.0, ue))), L, clamps);
+        a.E = clamp_energy(__dmul_rn(-bp.fission_t, emc_log(__dsub_rn(1.0, ue))), L, clamps);
     } else {
         int64_t i = resample_index(g, src.n, bp.pmax, src.u);
-        x = src.x[i]; y = src.y[i]; z = src.z[i];
-        dx = src.dx[i]; dy = src.dy[i]; dz = src.dz[i]; E = src.E[i];
+        a.x = src.x[i]; a.y = src.y[i]; a.z = src.z[i]; a.E = src.E[i];
+        b.dx = src.dx[i]; b.dy = src.dy[i]; b.dz = src.dz[i];
     }
+    b.rng = s;
+    P3 d;
     int32_t ax, mat;
-    int kd = locate_point(x, y, z, G, ax, mat);
-    S.rng[slot] = s; S.draws[slot] = draws; S.ordctr[slot] = 0; S.histlog[slot] = 0;
-    S.gid[slot] = g;
-    S.px[slot] = x; S.py[slot] = y; S.pz[slot] = z;
-    S.dx[slot] = dx; S.dy[slot] = dy; S.dz[slot] = dz; S.en[slot] = E;
-    S.kind[slot] = (int8_t)kd; S.axial[slot] = ax; S.mat[slot] = mat;
+    int kd = locate_point(a.x, a.y, a.z, G, ax, mat);
+    d.gid = g; d.draws = draws; d.ordctr = 0; d.histlog = 0; d.axial = ax; d.mat = mat;
+    d.surf = -1; d.kind = (int8_t)kd; d.pad = 0;
+    PState& p = S.ps[slot];
+    p.a = a; p.b = b; p.d = d;
     if (kd < 0) { set_error(ctl, nullptr, ERR_OUTSIDE_BOX, g); return false; }
     return true;
 }
@@ -92,44 +97,58 @@ __global__ void k_source_init(BatchP bp, DLib L, DGeom G, DSrc src, DSlots S, in
 
 // ----------------------------------------------------------------- sort ---
 
-// Coarse (material, log-energy) key: the sort only buys memory coherence for
-// the lookup (physics is sort-invariant, acceptance criterion 1), so ~0.2%
-// energy resolution is enough and keeps the radix sort to 3-4 passes.
-__global__ void k_sort_keys(const int32_t* __restrict__ q, int32_t n, const int32_t* __restrict__ mat,
-                            const double* __restrict__ en, uint32_t* __restrict__ keys, int e_bits)
+// Lookup-queue key (composition group, log E, material).  The sort only buys
+// memory coherence for the lookup (physics is sort-invariant, acceptance
+// criterion 1), so the top e_bits of the IEEE pattern (11 exponent +
+// e_bits-11 mantissa bits) suffice and keep the radix sort to 4 passes.
+// Group-major/energy-next puts particles of all fuel segments at similar
+// energy into the same warps (shared records); material is the minor key.
+__global__ void k_sort_keys(const int32_t* __restrict__ q, int32_t n, const PState* __restrict__ ps,
+                            DLib L, uint32_t* __restrict__ keys, int e_bits, int mat_bits, int mat_major)
 {
     int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int32_t s = q[i];
-    uint64_t eb = (uint64_t)__double_as_longlong(en[s]);          // E > 0: monotone bits
+    const int32_t m = ps[s].d.mat;
+    uint64_t eb = (uint64_t)__double_as_longlong(ps[s].a.E);          // E > 0: monotone bits
     uint32_t ek = (uint32_t)(eb >> (63 - e_bits)) & ((1u << e_bits) - 1u);
-    keys[i] = ((uint32_t)mat[s] << e_bits) | ek;
+    uint32_t mk = mat_bits ? ((uint32_t)m & ((1u << mat_bits) - 1u)) : 0u;
+    if (mat_major) keys[i] = (mk << e_bits) | ek;
+    else keys[i] = ((uint32_t)__ldg(L.mat_group + m) << (e_bits + mat_bits)) | (ek << mat_bits) | mk;
 }
 
 // --------------------------------------------------------------- lookup ---
 
 // K:573-710: macroscopic sigma_t/c/f/nu-sigma_f at the particle's energy in
 // its cell material, sequential fold in composition order.  One lane per
-// particle (the fold order is part of the bit-exact contract), sorted queue so
-// the 32 lanes of a warp share material and nearby grid brackets.
-__global__ void __launch_bounds__(256) k_lookup(const int32_t* __restrict__ q, int32_t n, DLib L,
+// particle (the fold order is part of the bit-exact contract); the queue is
+// sorted so the 32 lanes of a warp share material and nearby grid brackets.
+#ifndef EMC_LOOKUP_MINB
+#define EMC_LOOKUP_MINB 4
+#endif
+__global__ void __launch_bounds__(256, EMC_LOOKUP_MINB) k_lookup(const int32_t* __restrict__ q, int32_t n, DLib L,
                                                 DSlots S, int32_t fused, unsigned long long* cnt)
 {
-    unsigned long long interp = 0;
+    unsigned long long nl = 0;
     EMC_WARP_LOOP(n) {
         int64_t i = emc_base_ + lane_id();
         if (i < n) {
             int32_t s = q[i];
-            double E = S.en[s];
-            int32_t m = S.mat[s];
-            double st, sc, sf, snf;
-            macro_tcf(L, m, E, st, sc, sf, snf, fused ? S.ckpt + s : nullptr, S.nslots, S.nck);
-            S.cm_t[s] = st; S.cm_c[s] = sc; S.cm_f[s] = sf; S.cm_nsf[s] = snf;
-            interp += (unsigned long long)(__ldg(L.mat_off + m + 1) - __ldg(L.mat_off + m));
+            double E = S.ps[s].a.E;
+            int32_t m = S.ps[s].d.mat;
+            P2 c;
+#if EMC_LOOKUP_ILP > 0
+            macro_tcf_ilp<EMC_LOOKUP_ILP>(L, m, E, c.t, c.c, c.f, c.nsf,
+                                          fused ? S.ckpt + (int64_t)s * S.nck : nullptr, S.nck);
+#else
+            macro_tcf(L, m, E, c.t, c.c, c.f, c.nsf, fused ? S.ckpt + (int64_t)s * S.nck : nullptr, S.nck);
+#endif
+            S.ps[s].c = c;
+            nl += (unsigned long long)(__ldg(L.mat_off + m + 1) - __ldg(L.mat_off + m));
         }
     }
-    warp_add_u64(cnt + CNT_INTERP_TRANSPORT, 4ull * interp);
-    warp_add_u64(cnt + CNT_NUCLIDE_LOOKUPS, interp);
+    warp_add_u64(cnt + CNT_INTERP_TRANSPORT, 4ull * nl);
+    warp_add_u64(cnt + CNT_NUCLIDE_LOOKUPS, nl);
 }
 
 // -------------------------------------------------------------- advance ---
@@ -167,102 +186,91 @@ __global__ void __launch_bounds__(256) k_advance(const int32_t* __restrict__ q, 
         double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         int32_t base = 0;
         unsigned nlog = 0;
-        int64_t g = 0;
+        P3 d{};
         if (valid) {
-            g = S.gid[s];
-            double sig_t = S.cm_t[s];
+            PState& p = S.ps[s];
+            P0 a = p.a; P1 b = p.b; P2 c = p.c; d = p.d;
+            const double sig_t = c.t;
             if (!(sig_t > 0.0)) {
-                set_error(ctl, cnt, ERR_NONPOSITIVE_SIGMA, g);
-                valid = false;
-            }
-        }
-        if (valid) {
-            uint64_t rng = S.rng[s];
-            int32_t draws = S.draws[s];
-            double x = S.px[s], y = S.py[s], z = S.pz[s];
-            double dx = S.dx[s], dy = S.dy[s], dz = S.dz[s];
-            int kd = S.kind[s];
-            int32_t ax = S.axial[s];
-            double sig_t = S.cm_t[s];
-            double u = draw(rng, draws);
-            double d_coll = __ddiv_rn(-emc_log(__dsub_rn(1.0, u)), sig_t);
-            int32_t surf;
-            double dist = boundary_distance(x, y, z, dx, dy, dz, kd, ax, G, surf);
-            if (surf < 0) {
-                set_error(ctl, cnt, ERR_NO_SURFACE, g);
+                set_error(ctl, cnt, ERR_NONPOSITIVE_SIGMA, d.gid);
                 valid = false;
             } else {
-                bool crossing = !(d_coll < dist);
-                double ell = crossing ? dist : d_coll;
-                if (bp.score) {
-                    int32_t region = kd == KIND_FUEL ? ax : G.n_axial;
-                    base = region * 5;
-                    double fl = __dmul_rn(1.0, ell);     // wt == 1 (analog, K:950)
-                    if (bp.fused) {
-                        v[1] = __dmul_rn(fl, sig_t);
-                        v[2] = __dmul_rn(fl, __dadd_rn(S.cm_c[s], S.cm_f[s]));
-                        v[3] = __dmul_rn(fl, S.cm_f[s]);
-                        v[4] = __dmul_rn(fl, S.cm_nsf[s]);
-                    } else {   // K:757-765 naive re-assembly
-                        double st2, sc2, sf2, snf2;
-                        int32_t m = S.mat[s];
-                        macro_tcf(L, m, S.en[s], st2, sc2, sf2, snf2, nullptr, 0, 0);
-                        interp_score += 3ull * (unsigned long long)(__ldg(L.mat_off + m + 1) - __ldg(L.mat_off + m));
-                        v[1] = __dmul_rn(fl, st2);
-                        v[2] = __dmul_rn(fl, __dadd_rn(sc2, sf2));
-                        v[3] = __dmul_rn(fl, sf2);
-                        v[4] = __dmul_rn(fl, snf2);
-                    }
-                    v[0] = fl;
-                    #pragma unroll
-                    for (int k = 0; k < 5; ++k) nlog += v[k] != 0.0;
-                }
-                x = __dadd_rn(x, __dmul_rn(dx, ell));
-                y = __dadd_rn(y, __dmul_rn(dy, ell));
-                z = __dadd_rn(z, __dmul_rn(dz, ell));
-                S.px[s] = x; S.py[s] = y; S.pz[s] = z;
-                S.rng[s] = rng; S.draws[s] = draws;
-                S.surf[s] = surf;
-                if (draws >= kStride) {       // K:1159-1162
-                    set_error(ctl, cnt, ERR_STREAM_OVERLAP, g);
+                double u = draw(b.rng, d.draws);
+                double d_coll = __ddiv_rn(-emc_log(__dsub_rn(1.0, u)), sig_t);
+                int32_t surf;
+                double dist = boundary_distance(a.x, a.y, a.z, b.dx, b.dy, b.dz, d.kind, d.axial, G, surf);
+                if (surf < 0) {
+                    set_error(ctl, cnt, ERR_NO_SURFACE, d.gid);
                     valid = false;
                 } else {
-                    to_col = !crossing;
-                    to_cross = crossing;
+                    bool crossing = !(d_coll < dist);
+                    double ell = crossing ? dist : d_coll;
+                    if (bp.score) {
+                        int32_t region = d.kind == KIND_FUEL ? d.axial : G.n_axial;
+                        base = region * 5;
+                        double fl = __dmul_rn(1.0, ell);     // wt == 1 (analog, K:950)
+                        if (bp.fused) {
+                            v[1] = __dmul_rn(fl, sig_t);
+                            v[2] = __dmul_rn(fl, __dadd_rn(c.c, c.f));
+                            v[3] = __dmul_rn(fl, c.f);
+                            v[4] = __dmul_rn(fl, c.nsf);
+                        } else {   // K:757-765 naive re-assembly
+                            double st2, sc2, sf2, snf2;
+                            macro_tcf_simple(L, d.mat, a.E, st2, sc2, sf2, snf2, nullptr, 0);
+                            interp_score += 3ull * (unsigned long long)(__ldg(L.mat_off + d.mat + 1) -
+                                                                        __ldg(L.mat_off + d.mat));
+                            v[1] = __dmul_rn(fl, st2);
+                            v[2] = __dmul_rn(fl, __dadd_rn(sc2, sf2));
+                            v[3] = __dmul_rn(fl, sf2);
+                            v[4] = __dmul_rn(fl, snf2);
+                        }
+                        v[0] = fl;
+                        #pragma unroll
+                        for (int k = 0; k < 5; ++k) nlog += v[k] != 0.0;
+                    }
+                    a.x = __dadd_rn(a.x, __dmul_rn(b.dx, ell));
+                    a.y = __dadd_rn(a.y, __dmul_rn(b.dy, ell));
+                    a.z = __dadd_rn(a.z, __dmul_rn(b.dz, ell));
+                    d.surf = (int16_t)surf;
+                    if (d.draws >= kStride) {       // K:1159-1162
+                        set_error(ctl, cnt, ERR_STREAM_OVERLAP, d.gid);
+                        valid = false;
+                    } else {
+                        to_col = !crossing;
+                        to_cross = crossing;
+                    }
+                    p.a = a; p.b = b;
                 }
             }
         }
-        if (bp.score) {
-            if (bp.use_logs) {
-                unsigned want = (valid || to_col || to_cross) ? nlog : 0u;
-                unsigned long long at = warp_claim(&ctl->log_n, want);
-                if (want) {
-                    if (at + want > (unsigned long long)lg.cap) {
-                        atomicExch(&ctl->ovf, 1);
-                    } else {
-                        int32_t o = S.ordctr[s];
-                        unsigned j = 0;
-                        #pragma unroll
-                        for (int k = 0; k < 5; ++k) {
-                            if (v[k] != 0.0) {
-                                lg.gid[at + j] = g; lg.ord[at + j] = o + (int32_t)j;
-                                lg.bin[at + j] = base + k; lg.val[at + j] = v[k];
-                                ++j;
-                            }
+        if (bp.score && bp.use_logs) {
+            unsigned want = (to_col || to_cross) ? nlog : 0u;
+            unsigned long long at = warp_claim(&ctl->log_n, want);
+            if (want) {
+                if (at + want > (unsigned long long)lg.cap) {
+                    atomicExch(&ctl->ovf, 1);
+                } else {
+                    unsigned j = 0;
+                    #pragma unroll
+                    for (int k = 0; k < 5; ++k) {
+                        if (v[k] != 0.0) {
+                            lg.gid[at + j] = d.gid; lg.ord[at + j] = d.ordctr + (int32_t)j;
+                            lg.bin[at + j] = base + k; lg.val[at + j] = v[k];
+                            ++j;
                         }
                     }
-                    S.ordctr[s] += (int32_t)want;
-                    int32_t h = S.histlog[s] + (int32_t)want;
-                    S.histlog[s] = h;
-                    if (h > kMaxHistLog) {
-                        set_error(ctl, cnt, ERR_RUNAWAY_HISTORY, g);
-                        to_col = to_cross = false;
-                    }
                 }
-            } else {
-                score_bins(bins, to_col || to_cross, base, v);
+                d.ordctr += (int32_t)want;
+                d.histlog += (int32_t)want;
+                if (d.histlog > kMaxHistLog) {
+                    set_error(ctl, cnt, ERR_RUNAWAY_HISTORY, d.gid);
+                    to_col = to_cross = false;
+                }
             }
+        } else if (bp.score) {
+            score_bins(bins, to_col || to_cross, base, v);
         }
+        if (to_col || to_cross) S.ps[s].d = d;
         queue_push(q_col, &ctl->nC, s, to_col);
         queue_push(q_cross, &ctl->nX, s, to_cross);
     }
@@ -282,30 +290,26 @@ __global__ void __launch_bounds__(256) k_crossing(const int32_t* __restrict__ q,
         bool valid = i < n;
         int32_t s = valid ? q[i] : 0;
         if (valid) {
-            int32_t surf = S.surf[s];
-            double x = S.px[s], y = S.py[s], z = S.pz[s];
-            double dx = S.dx[s], dy = S.dy[s], dz = S.dz[s];
-            int kd = S.kind[s];
-            int32_t ax = S.axial[s];
+            PState& p = S.ps[s];
+            P0 a = p.a; P1 b = p.b; P3 d = p.d;
+            const int32_t surf = d.surf;
             if (surf >= SURF_XMIN && surf <= SURF_ZMAX) {
-                if (surf == SURF_XMIN || surf == SURF_XMAX) dx = -dx;
-                else if (surf == SURF_YMIN || surf == SURF_YMAX) dy = -dy;
-                else dz = -dz;
+                if (surf == SURF_XMIN || surf == SURF_XMAX) b.dx = -b.dx;
+                else if (surf == SURF_YMIN || surf == SURF_YMAX) b.dy = -b.dy;
+                else b.dz = -b.dz;
             }
-            x = __dadd_rn(x, __dmul_rn(dx, kNudge));
-            y = __dadd_rn(y, __dmul_rn(dy, kNudge));
-            z = __dadd_rn(z, __dmul_rn(dz, kNudge));
+            a.x = __dadd_rn(a.x, __dmul_rn(b.dx, kNudge));
+            a.y = __dadd_rn(a.y, __dmul_rn(b.dy, kNudge));
+            a.z = __dadd_rn(a.z, __dmul_rn(b.dz, kNudge));
             if (surf == SURF_CYL) {
-                if (kd == KIND_FUEL) { kd = KIND_MOD; ax = -1; }
-                else { kd = KIND_FUEL; ax = axial_index(z, G.n_axial, G.height); }
+                if (d.kind == KIND_FUEL) { d.kind = KIND_MOD; d.axial = -1; }
+                else { d.kind = KIND_FUEL; d.axial = axial_index(a.z, G.n_axial, G.height); }
             } else if (surf >= SURF_AXIAL_BASE) {
                 int32_t jpl = surf - SURF_AXIAL_BASE;
-                ax = dz > 0.0 ? jpl : jpl - 1;
+                d.axial = b.dz > 0.0 ? jpl : jpl - 1;
             }
-            S.px[s] = x; S.py[s] = y; S.pz[s] = z;
-            S.dx[s] = dx; S.dy[s] = dy; S.dz[s] = dz;
-            S.kind[s] = (int8_t)kd; S.axial[s] = ax;
-            S.mat[s] = kd == KIND_FUEL ? G.fuel_mats[ax] : G.mod_mat;
+            d.mat = d.kind == KIND_FUEL ? G.fuel_mats[d.axial] : G.mod_mat;
+            p.a = a; p.b = b; p.d = d;
         }
         queue_push(q_next, &ctl->nL2, s, valid);
     }
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(256) k_crossing(const int32_t* __restrict__ q,
 // last sigma_t prefix checkpoint <= target written by the lookup, so at most
 // kCkptStride partials are re-interpolated (bit-identical to the stored
 // part_t walk).  Naive: re-interpolate from the first nuclide (K:853-883).
-__device__ __forceinline__ int32_t select_nuclide(const DLib& L, const DSlots& S, int32_t s, int32_t e0,
+__device__ __forceinline__ int32_t select_nuclide(const DLib& L, const double* ck, int32_t nck, int32_t e0,
                                                   int32_t e1, int32_t bin, double E, double tgt,
                                                   bool fused, double& pt_sel, unsigned long long& interp)
 {
@@ -326,15 +330,14 @@ __device__ __forceinline__ int32_t select_nuclide(const DLib& L, const DSlots& S
     double cum = 0.0;
     if (fused && ncomp > kCkptStride) {
         int32_t cmax = (ncomp - 1) / kCkptStride;
-        if (cmax > S.nck) cmax = S.nck;
+        if (cmax > nck) cmax = nck;
         int32_t lo = 0, hi = cmax;      // largest c with P_c <= tgt (P_0 = 0)
         while (lo < hi) {
             int32_t mid = (lo + hi + 1) >> 1;
-            double p = S.ckpt[(int64_t)(mid - 1) * S.nslots + s];
-            if (p <= tgt) lo = mid; else hi = mid - 1;
+            if (ck[mid - 1] <= tgt) lo = mid; else hi = mid - 1;
         }
         c = lo;
-        if (c > 0) cum = S.ckpt[(int64_t)(c - 1) * S.nslots + s];
+        if (c > 0) cum = ck[c - 1];
     }
     int32_t ksel = e1 - 1;
     pt_sel = 0.0;
@@ -365,53 +368,46 @@ __global__ void __launch_bounds__(256) k_collision(const int32_t* __restrict__ q
         int32_t s = valid ? q[i] : 0;
         bool alive = false, died = false;
         double kval = 0.0;
-        int64_t g = 0;
         unsigned nsites = 0;
-        uint64_t rng = 0;
-        int32_t draws = 0;
-        double x = 0, y = 0, z = 0, E = 0;
-        int32_t ksel_nid = 0;
+        P0 a{}; P1 b{}; P3 d{};
         if (valid) {
-            g = S.gid[s];
-            double st = S.cm_t[s];
-            kval = __dmul_rn(1.0, __ddiv_rn(S.cm_nsf[s], st));    // wt * (nsf / st)
-            rng = S.rng[s]; draws = S.draws[s];
-            E = S.en[s];
-            int32_t m = S.mat[s];
-            int32_t e0 = __ldg(L.mat_off + m), e1 = __ldg(L.mat_off + m + 1);
-            int32_t bin = energy_bin(E, L);
-            double u1 = draw(rng, draws);
+            PState& p = S.ps[s];
+            a = p.a; b = p.b; d = p.d;
+            const P2 c = p.c;
+            const double st = c.t;
+            kval = __dmul_rn(1.0, __ddiv_rn(c.nsf, st));            // wt * (nsf / st)
+            const double E = a.E;
+            const int32_t e0 = __ldg(L.mat_off + d.mat), e1 = __ldg(L.mat_off + d.mat + 1);
+            const int32_t bin = energy_bin(E, L);
+            double u1 = draw(b.rng, d.draws);
             double tgt = __dmul_rn(u1, st);
             double pt_sel;
-            int32_t ksel = select_nuclide(L, S, s, e0, e1, bin, E, tgt, bp.fused != 0, pt_sel, interp);
+            int32_t ksel = select_nuclide(L, S.ckpt + (int64_t)s * S.nck, S.nck, e0, e1, bin, E, tgt,
+                                          bp.fused != 0, pt_sel, interp);
             const Comp cs = L.comp[ksel];
-            ksel_nid = cs.nid;
             double s_s, s_c, s_f;
             micro_scf(L, cs, bin, E, s_s, s_c, s_f);
             interp += 3;
-            double ps = __dmul_rn(cs.den, s_s), pc = __dmul_rn(cs.den, s_c);
-            double u2 = draw(rng, draws);
+            double ps_ = __dmul_rn(cs.den, s_s), pc = __dmul_rn(cs.den, s_c);
+            double u2 = draw(b.rng, d.draws);
             double tgt2 = __dmul_rn(u2, pt_sel);
-            if (tgt2 < ps) {                                     // scatter
-                double u3 = draw(rng, draws), u4 = draw(rng, draws);
-                double nx, ny, nz;
-                isotropic(u3, u4, nx, ny, nz);
-                S.dx[s] = nx; S.dy[s] = ny; S.dz[s] = nz;
-                double u5 = draw(rng, draws);
+            if (tgt2 < ps_) {                                    // scatter
+                double u3 = draw(b.rng, d.draws), u4 = draw(b.rng, d.draws);
+                isotropic(u3, u4, b.dx, b.dy, b.dz);
+                double u5 = draw(b.rng, d.draws);
                 double ep = __dmul_rn(E, __dadd_rn(bp.alpha, __dmul_rn(__dsub_rn(1.0, bp.alpha), u5)));
-                S.en[s] = clamp_energy(ep, L, clamps);
+                a.E = clamp_energy(ep, L, clamps);
                 alive = true;
-            } else if (tgt2 < __dadd_rn(ps, pc)) {              // capture
+            } else if (tgt2 < __dadd_rn(ps_, pc)) {             // capture
                 captures += 1;
                 died = true;
             } else {                                             // fission
                 fissions += 1;
                 died = true;
-                double u5 = draw(rng, draws);
-                double nu_sel = __ldg(L.nu + ksel_nid);
+                double u5 = draw(b.rng, d.draws);
+                double nu_sel = __ldg(L.nu + cs.nid);
                 int64_t ns = (int64_t)floor(__dadd_rn(__ddiv_rn(nu_sel, bp.k_run), u5));
                 nsites = ns > 0 ? (unsigned)ns : 0u;
-                x = S.px[s]; y = S.py[s]; z = S.pz[s];
             }
         }
         // contribution to the k-effective bin (every batch), K:829-834
@@ -420,13 +416,10 @@ __global__ void __launch_bounds__(256) k_collision(const int32_t* __restrict__ q
             unsigned long long at = warp_claim(&ctl->log_n, want);
             if (want) {
                 if (at + 1 > (unsigned long long)lg.cap) atomicExch(&ctl->ovf, 1);
-                else {
-                    lg.gid[at] = g; lg.ord[at] = S.ordctr[s]; lg.bin[at] = bp.kbin; lg.val[at] = kval;
-                }
-                S.ordctr[s] += 1;
-                int32_t h = S.histlog[s] + 1;
-                S.histlog[s] = h;
-                if (h > kMaxHistLog) { set_error(ctl, cnt, ERR_RUNAWAY_HISTORY, g); alive = died = false; }
+                else { lg.gid[at] = d.gid; lg.ord[at] = d.ordctr; lg.bin[at] = bp.kbin; lg.val[at] = kval; }
+                d.ordctr += 1;
+                d.histlog += 1;
+                if (d.histlog > kMaxHistLog) { set_error(ctl, cnt, ERR_RUNAWAY_HISTORY, d.gid); alive = died = false; }
             }
         } else {
             warp_add_f64(bins + bp.kbin, valid ? kval : 0.0);
@@ -434,28 +427,29 @@ __global__ void __launch_bounds__(256) k_collision(const int32_t* __restrict__ q
         // fission sites (K:913-922); the site draws continue the parent stream
         unsigned long long at = warp_claim(&ctl->site_n, nsites);
         for (unsigned ms = 0; ms < nsites; ++ms) {
-            double ua = draw(rng, draws), ub = draw(rng, draws);
+            double ua = draw(b.rng, d.draws), ub = draw(b.rng, d.draws);
             double sx, sy, sz;
             isotropic(ua, ub, sx, sy, sz);
-            double uc = draw(rng, draws);
+            double uc = draw(b.rng, d.draws);
             double es = clamp_energy(__dmul_rn(-bp.fission_t, emc_log(__dsub_rn(1.0, uc))), L, clamps);
             unsigned long long w = at + ms;
             if (w >= (unsigned long long)sb.cap) { atomicExch(&ctl->ovf, 2); continue; }
-            sb.parent[w] = g; sb.ord[w] = (int32_t)ms;
-            sb.x[w] = x; sb.y[w] = y; sb.z[w] = z;
+            sb.parent[w] = d.gid; sb.ord[w] = (int32_t)ms;
+            sb.x[w] = a.x; sb.y[w] = a.y; sb.z[w] = a.z;
             sb.dx[w] = sx; sb.dy[w] = sy; sb.dz[w] = sz; sb.E[w] = es;
         }
-        if (valid && (alive || died)) {
-            S.rng[s] = rng; S.draws[s] = draws;
-            if (draws >= kStride) {                              // K:1183-1186
-                set_error(ctl, cnt, ERR_STREAM_OVERLAP, g);
-                alive = died = false;
-            }
+        if (valid && (alive || died) && d.draws >= kStride) {      // K:1183-1186
+            set_error(ctl, cnt, ERR_STREAM_OVERLAP, d.gid);
+            alive = died = false;
+        }
+        if (alive) {
+            PState& p = S.ps[s];
+            p.a = a; p.b = b; p.d = d;
         }
         bool refill = false;
         if (died) {                                              // K:999-1006
-            maxdraws = max(maxdraws, (unsigned long long)draws);
-            maxhist = max(maxhist, (unsigned long long)S.histlog[s]);
+            maxdraws = max(maxdraws, (unsigned long long)d.draws);
+            maxhist = max(maxhist, (unsigned long long)d.histlog);
         }
         // claim the next source particle for dead slots
         unsigned long long idx = warp_claim(&ctl->cursor, died ? 1u : 0u);
