@@ -305,11 +305,18 @@ class OracleError(Exception):
         self.kind = kind
 
 
+DEFAULTS = dict(max_in_flight=10000, tally_mode="fused", reduction="deterministic",
+                sort_enabled=True, sort_every_n=1, workers=1, seed=42, alpha_scatter=0.5,
+                fission_temperature=1.3e6, perturb_particle=-1, mode="event")
+
+
 def run(cfg: dict, lib_arrays, geom, workers: int | None = None,
         batches: range | None = None) -> dict:
     """Restatement of run_replicated (R:155-315).  ``cfg`` holds the RunConfig
-    fields by name.  Returns keff values, batch sums, final bank, counters,
-    timings and the active/inactive rates."""
+    fields by name (missing ones take RunConfig's defaults, T:30-45).
+    Returns keff values, batch sums, final bank, counters, timings and the
+    active/inactive rates."""
+    cfg = dict(DEFAULTS, **cfg)
     olib = OracleLibrary(lib_arrays)
     ogeom = OracleGeometry(geom)
     ppb = int(cfg["particles_per_batch"])

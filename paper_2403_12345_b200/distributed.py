@@ -67,9 +67,9 @@ def allgather_array(world: World, arr: np.ndarray) -> np.ndarray:
     import torch
     import torch.distributed as dist
     t = torch.as_tensor(np.ascontiguousarray(arr)).to(_tensor_device(world))
-    out = torch.empty((world.size,) + tuple(t.shape), dtype=t.dtype, device=t.device)
-    dist.all_gather_into_tensor(out, t)
-    return out.cpu().numpy()
+    parts = [torch.empty_like(t) for _ in range(world.size)]
+    dist.all_gather(parts, t)
+    return torch.stack(parts).cpu().numpy()
 
 
 def combine_counters(per_rank: np.ndarray, sums, maxes) -> dict:
@@ -136,9 +136,9 @@ def gather_bank(world: World, local_cols, counts: np.ndarray):
         n = int(counts[world.rank])
         if n:
             padded[:n] = col[:n].to(dev)
-        gathered = torch.empty((world.size, max(mx, 1)), dtype=col.dtype, device=dev)
-        dist.all_gather_into_tensor(gathered, padded)
-        out.append(torch.cat([gathered[r, :int(counts[r])] for r in range(world.size)]))
+        parts = [torch.empty_like(padded) for _ in range(world.size)]
+        dist.all_gather(parts, padded)
+        out.append(torch.cat([parts[r][:int(counts[r])] for r in range(world.size)]))
     return out
 
 

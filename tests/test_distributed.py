@@ -1,0 +1,95 @@
+"""Multi-rank coordinator logic over torch.distributed (gloo, world size 2,
+CPU): rank partitioning, counter combination, rank-ordered fast reduction,
+the chained deterministic fold (must equal a single-rank left fold bit for
+bit) and the bank all-gather (rank-ordered concatenation)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+from paper_2403_12345_b200 import distributed as D  # noqa: E402
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = D.current_world()
+        assert (w.rank, w.size, w.device_backend) == (rank, world, False)
+        rng = np.random.RandomState(7)
+        n_bins = 11
+        # per-rank contribution logs already in canonical (bin, gid, ord) order
+        vals = [rng.uniform(0.1, 2.0, 40) for _ in range(world)]
+        bins = [rng.randint(0, n_bins, 40) for _ in range(world)]
+
+        def fold_local(init):
+            out = np.zeros(n_bins) if init is None else init.copy()
+            for b, v in zip(bins[rank], vals[rank]):
+                out[b] += v
+            return out
+        chained = D.chained_fold(w, fold_local, n_bins)
+        ref = np.zeros(n_bins)
+        for r in range(world):
+            for b, v in zip(bins[r], vals[r]):
+                ref[b] += v
+        ok_chain = np.array_equal(chained, ref)
+
+        local = np.full(n_bins, float(rank + 1))
+        fast = D.fast_bins(w, local)
+        ok_fast = np.array_equal(fast, sum(np.full(n_bins, float(r + 1)) for r in range(world)))
+
+        counts = np.array([3, 5][:world], np.int64)
+        n = counts[rank]
+        lo = int(counts[:rank].sum())
+        cols = [torch.arange(lo, lo + n, dtype=torch.int64), torch.zeros(n, dtype=torch.int32)] + \
+            [torch.full((n,), float(rank)) for _ in range(7)]
+        g = D.gather_bank(w, cols, counts)
+        ok_bank = g[0].tolist() == list(range(int(counts.sum()))) and \
+            g[2].tolist() == [0.0] * 3 + [1.0] * 5
+
+        per_rank = D.allgather_array(w, np.array([rank + 1, 10 * (rank + 1)], np.int64))
+        comb = D.combine_counters(per_rank, (("s", 0),), (("m", 1),))
+        ok_cnt = comb == {"s": 3, "m": 20}
+        q.put((rank, ok_chain, ok_fast, ok_bank, ok_cnt))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_collectives():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(2))
+    for rank, *oks in res:
+        assert all(oks), (rank, oks)
+
+
+def test_block_partition_covers_batch():
+    for ppb in (1, 7, 100, 40_000_003):
+        for w in (1, 2, 3, 8):
+            if w > ppb:
+                continue
+            blocks = [D.block_of(r, w, ppb) for r in range(w)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == ppb
+            assert all(a[1] == b[0] for a, b in zip(blocks, blocks[1:]))
