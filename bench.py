@@ -143,7 +143,7 @@ def run_reference(args):
     from paper_2403_12345_b200.presets import depleted_pincell
     lib, cell = depleted_pincell(272, 3, 11303, 100, seed=1)
     threads = os.cpu_count() or 1
-    ppb = args.ref_particles or 1500 * threads
+    ppb = args.ref_particles or 3000 * threads
     from oracle import driver
     cfg = dict(particles_per_batch=ppb, inactive_batches=args.warmup, active_batches=args.steps,
                mode="event", max_in_flight=10000, tally_mode="fused", reduction="deterministic",
@@ -154,7 +154,10 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * res["active_wall"] / max(args.steps, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": dict(WORKLOAD, ppb_sample=ppb),
+            "data": "synthetic",
+            "config": dict(WORKLOAD, reduction="deterministic (reference default)", ppb_sample=ppb,
+                           impl="C restatement of the reference kernels (oracle/, bit-exact with the "
+                                "numba reference on this image's glibc)"),
             "cpu_baseline": {"value": v, "unit": "particles/s", "cores": threads, "kind": "port",
                              "sample": f"{ppb} particles/batch x ({args.warmup}+{args.steps}) batches"},
             "e2e": {"value": v, "unit": "particles/s", "h2d_bytes_per_step": 0,
