@@ -129,7 +129,11 @@ struct emc_ctx {
     bool mat_major = true;
 
     // particle slots
-    DBuf<PState> ps; DBuf<double> ckpt;
+    // particle lines, double-buffered: after each lookup-queue sort the lines
+    // are permuted into queue order (k_reorder), so every later sweep streams
+    DBuf<PState> ps, ps2; DBuf<double> ckpt; DBuf<int32_t> iota;
+    PState* ps_cur = nullptr;
+    bool reorder = true;
     DSlots S{};
 
     // queues + sort scratch
@@ -197,7 +201,7 @@ extern "C" void emc_destroy(emc_ctx* c)
     for (auto* b : {&c->mat_off, &c->hash, &c->fuel_mats, &c->qa, &c->qb, &c->qs, &c->qc, &c->qx,
                     &c->bidx_in, &c->bidx_out, &c->lg_ord, &c->lg_bin})
         b->release();
-    c->ps.release(); c->rec.release(); c->comp.release();
+    c->ps.release(); c->ps2.release(); c->iota.release(); c->rec.release(); c->comp.release();
     c->mat_group.release(); c->grp_off.release(); c->gnuc.release(); c->ddT.release();
     c->keys_in.release(); c->keys_out.release(); c->cub_tmp.release();
     c->bkey_in.release(); c->bkey_out.release(); c->lkey_in.release(); c->lkey_out.release();
@@ -378,13 +382,24 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
     c->nck = cfg->fused ? std::max(0, (c->max_comp - 1) / kCkptStride) : 0;
     int rc = 0;
     rc |= c->ps.alloc(nslots);
+    const char* ro = getenv("EMC_REORDER");
+    c->reorder = !(ro && ro[0] == '0');
+    if (c->reorder) rc |= c->ps2.alloc(nslots);
+    rc |= c->iota.alloc(nslots);
     rc |= c->ckpt.alloc(std::max<int64_t>(1, (int64_t)c->nck * nslots));
     for (auto* b : {&c->qa, &c->qb, &c->qs, &c->qc, &c->qx})
         rc |= b->alloc(nslots);
     rc |= c->keys_in.alloc(nslots); rc |= c->keys_out.alloc(nslots);
     rc |= c->bins.alloc(c->n_bins); rc |= c->bins_init.alloc(c->n_bins); rc |= c->bins_out.alloc(c->n_bins);
     if (rc) return EMC_E_OOM;
-    c->S = DSlots{c->ps.p, c->ckpt.p, nslots, c->nck};
+    if (rc) return EMC_E_OOM;
+    {
+        std::vector<int32_t> h(nslots);
+        for (int64_t i = 0; i < nslots; ++i) h[i] = (int32_t)i;
+        EMC_TRY_CUDA(cudaMemcpy(c->iota.p, h.data(), nslots * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    c->ps_cur = c->ps.p;
+    c->S = DSlots{c->ps_cur, c->ckpt.p, nslots, c->nck};
     // fission bank: reference starts at n_assigned*6+1024 (R:92); ~1 site per
     // source particle is typical, so start at 2x and grow on overflow.
     if ((rc = alloc_sites(c, (size_t)(cfg->n_assigned * 2 + 4096)))) return rc;
@@ -537,7 +552,7 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             bool do_sort = cf.sort_enabled && nL > 1 && (look_inv % cf.sort_every) == 0;
             EMC_TRY_CUDA(cudaEventRecord(c->ev[0], st));
             if (do_sort) {
-                k_sort_keys<<<grid_for(nL, BLK, 1 << 30), BLK, 0, st>>>(cur, (int32_t)nL, c->ps.p, c->L,
+                k_sort_keys<<<grid_for(nL, BLK, 1 << 30), BLK, 0, st>>>(cur, (int32_t)nL, c->ps_cur, c->L,
                                                                         c->keys_in.p, c->e_bits, c->mat_bits,
                                                                         c->mat_major);
                 EMC_CHECK_LAUNCH(c);
@@ -546,6 +561,14 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
                 if (rc) return rc;
                 q = c->qs.p;
                 host_cnt[CNT_SORTS] += 1;
+                if (c->reorder) {
+                    PState* dst = c->ps_cur == c->ps.p ? c->ps2.p : c->ps.p;
+                    k_reorder<<<grid_for(nL, BLK, 1 << 30), BLK, 0, st>>>(c->qs.p, (int32_t)nL, c->ps_cur, dst);
+                    EMC_CHECK_LAUNCH(c);
+                    c->ps_cur = dst;
+                    c->S.ps = dst;
+                    q = c->iota.p;
+                }
             }
             look_inv++;
             EMC_TRY_CUDA(cudaEventRecord(c->ev[1], st));

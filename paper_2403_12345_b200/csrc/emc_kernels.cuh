@@ -117,6 +117,18 @@ __global__ void k_sort_keys(const int32_t* __restrict__ q, int32_t n, const PSta
     else keys[i] = ((uint32_t)__ldg(L.mat_group + m) << (e_bits + mat_bits)) | (ek << mat_bits) | mk;
 }
 
+// Permute particle lines into sorted queue order (dst[i] = src[perm[i]]):
+// one random 128-byte line read + one streamed write per particle, after
+// which lookup/advance address slot i directly and crossing/collision walk
+// near-monotone subsequences.  Physics is slot-invariant.
+__global__ void __launch_bounds__(256) k_reorder(const int32_t* __restrict__ perm, int32_t n,
+                                                 const PState* __restrict__ src, PState* __restrict__ dst)
+{
+    int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    dst[i] = src[perm[i]];
+}
+
 // --------------------------------------------------------------- lookup ---
 
 // K:573-710: macroscopic sigma_t/c/f/nu-sigma_f at the particle's energy in
