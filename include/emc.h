@@ -159,6 +159,12 @@ int emc_lcg_skip(emc_ctx *ctx, int64_t n, const uint64_t *state, const uint64_t 
 /* device log/sin/cos replicas (emc_libm.h): out[n][3] */
 int emc_libm_eval(emc_ctx *ctx, int64_t n, const double *x, double *out);
 
+/* tuning harness: mean ms of the XS-lookup microbenchmark kernel over n
+ * (material, energy) pairs; variant 0 = production arithmetic, 1-3 = timing
+ * ablations (no division / shared energy / no gathers; wrong values) */
+int emc_bench_lookup(emc_ctx *ctx, int64_t n, const int32_t *mats, const double *E, int32_t variant,
+                     int32_t iters, double *ms, double *checksum);
+
 /* number of kernel launches issued by this context so far */
 int64_t emc_launch_count(emc_ctx *ctx);
 

@@ -125,8 +125,8 @@ struct emc_ctx {
     bool configured = false;
     emc_run_config cfg{};
     int64_t nslots = 0;
-    int32_t nck = 0, n_bins = 0, kbin = 0, e_bits = 20, mat_bits = 1, grp_bits = 0;
-    bool mat_major = true;
+    int32_t nck = 0, n_bins = 0, kbin = 0, mat_bits = 1, grp_bits = 0, band_bits = 0, ebin_bits = 0;
+    int32_t n_bands = 1, key_bits = 1, ebin_shift = 0;
 
     // particle slots
     // particle lines, double-buffered: after each lookup-queue sort the lines
@@ -134,6 +134,7 @@ struct emc_ctx {
     DBuf<PState> ps, ps2; DBuf<double> ckpt; DBuf<int32_t> iota;
     PState* ps_cur = nullptr;
     bool reorder = true;
+    int lookup_block = 1024;
     DSlots S{};
 
     // queues + sort scratch
@@ -259,6 +260,7 @@ extern "C" int emc_upload_library(emc_ctx* c, const emc_library* lib)
     for (int64_t i = 0; i < nn; ++i) gmax = std::max<int64_t>(gmax, lib->grid_off[i + 1] - lib->grid_off[i]);
     double octaves = std::max(1.0, std::log2(hi / lo));
     int mbits = (int)std::ceil(std::log2(std::max(1.0, (double)gmax / octaves)));
+    if (const char* hb = getenv("EMC_HASH_EXTRA_BITS")) mbits += atoi(hb);   // tuning knob
     mbits = std::min(std::max(mbits, 0), 16);
     int shift = 52 - mbits;
     uint64_t blo, bhi;
@@ -382,6 +384,7 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
     c->nck = cfg->fused ? std::max(0, (c->max_comp - 1) / kCkptStride) : 0;
     int rc = 0;
     rc |= c->ps.alloc(nslots);
+    if (const char* lb = getenv("EMC_LOOKUP_BLOCK")) c->lookup_block = atoi(lb);
     const char* ro = getenv("EMC_REORDER");
     c->reorder = !(ro && ro[0] == '0');
     if (c->reorder) rc |= c->ps2.alloc(nslots);
@@ -406,21 +409,27 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
     if (cfg->use_logs) {
         if ((rc = alloc_logs(c, (size_t)(cfg->n_assigned * 64 + 4096)))) return rc;
     }
-    // lookup sort key (32 bits): composition group | log-energy | material.
-    // Energy-major inside a group: all fuel segments share one nuclide list,
-    // so neighbouring lanes read the same grid records (see DLib).
-    int gb = 0;
-    while ((1 << gb) < c->n_groups) ++gb;
-    int mb = 0;
-    while ((1 << mb) < c->n_materials) ++mb;
-    mb = std::min(mb, 32 - gb - 16);
-    c->grp_bits = gb;
-    c->mat_bits = mb;
-    c->e_bits = std::min(24, 32 - gb - mb);
-    // EMC_SORT_MODE=material: material-major key (mat, log E) instead
-    const char* sm = getenv("EMC_SORT_MODE");
-    c->mat_major = !(sm && std::string(sm) == "energy");
-    if (c->mat_major) { c->grp_bits = 0; c->mat_bits = mb; c->e_bits = std::min(24, 32 - mb); }
+    // lookup sort key (32 bits): group | energy band | material | energy bin
+    // (see k_sort_keys).  EMC_SORT_BANDS overrides the band count (1 = pure
+    // material-major order).
+    {
+        auto bits = [](int64_t v) { int b = 0; while (((int64_t)1 << b) < v) ++b; return b; };
+        int nb = 64;
+        if (const char* e = getenv("EMC_SORT_BANDS")) nb = std::max(1, atoi(e));
+        c->n_bands = nb;
+        c->grp_bits = bits(c->n_groups);
+        c->band_bits = bits(nb);
+        c->mat_bits = bits(c->n_materials);
+        c->ebin_bits = bits(c->L.nbins);
+        int total = c->grp_bits + c->band_bits + c->mat_bits + c->ebin_bits;
+        if (total > 32) {            // drop fine-energy bits first (order stays valid)
+            c->ebin_bits = std::max(0, c->ebin_bits - (total - 32));
+            total = c->grp_bits + c->band_bits + c->mat_bits + c->ebin_bits;
+        }
+        if (total > 32) { g_err = "too many materials/groups for the 32-bit sort key"; return EMC_E_RANGE; }
+        c->key_bits = total;
+        c->ebin_shift = bits(c->L.nbins) - c->ebin_bits;
+    }
     int gidb = 1;
     while (((int64_t)1 << gidb) < cfg->n_assigned) ++gidb;
     c->gid_bits = gidb;
@@ -553,11 +562,10 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             EMC_TRY_CUDA(cudaEventRecord(c->ev[0], st));
             if (do_sort) {
                 k_sort_keys<<<grid_for(nL, BLK, 1 << 30), BLK, 0, st>>>(cur, (int32_t)nL, c->ps_cur, c->L,
-                                                                        c->keys_in.p, c->e_bits, c->mat_bits,
-                                                                        c->mat_major);
+                                                                        c->keys_in.p, c->ebin_bits, c->ebin_shift,
+                                                                        c->mat_bits, c->band_bits, c->n_bands);
                 EMC_CHECK_LAUNCH(c);
-                int rc = sort_cub(c, c->keys_in.p, c->keys_out.p, cur, c->qs.p, (int)nL,
-                                  c->grp_bits + c->e_bits + c->mat_bits);
+                int rc = sort_cub(c, c->keys_in.p, c->keys_out.p, cur, c->qs.p, (int)nL, c->key_bits);
                 if (rc) return rc;
                 q = c->qs.p;
                 host_cnt[CNT_SORTS] += 1;
@@ -572,7 +580,19 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             }
             look_inv++;
             EMC_TRY_CUDA(cudaEventRecord(c->ev[1], st));
-            k_lookup<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(q, (int32_t)nL, c->L, c->S, cf.fused, c->cnt.p);
+            switch (c->lookup_block) {
+            case 1024:
+                k_lookup<1024><<<grid_for(nL, 1024, c->sm_count), 1024, 0, st>>>(q, (int32_t)nL, c->L, c->S,
+                                                                                 cf.fused, c->cnt.p);
+                break;
+            case 512:
+                k_lookup<512><<<grid_for(nL, 512, 2 * c->sm_count), 512, 0, st>>>(q, (int32_t)nL, c->L, c->S,
+                                                                                  cf.fused, c->cnt.p);
+                break;
+            default:
+                k_lookup<256><<<grid_for(nL, 256, maxb), 256, 0, st>>>(q, (int32_t)nL, c->L, c->S, cf.fused,
+                                                                       c->cnt.p);
+            }
             EMC_CHECK_LAUNCH(c);
             EMC_TRY_CUDA(cudaEventRecord(c->ev[2], st));
             k_advance<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(q, (int32_t)nL, bp, c->L, c->G, c->S, lg, c->bins.p,
@@ -950,5 +970,46 @@ extern "C" int emc_libm_eval(emc_ctx* c, int64_t n, const double* x, double* out
     to_host(out, dout, 3 * n, st);
     EMC_TRY_CUDA(cudaStreamSynchronize(st));
     dx.release(); dout.release();
+    return 0;
+}
+
+// test/tuning entry point: time k_lookup_bench<variant> over n (mat, E) pairs
+extern "C" int emc_bench_lookup(emc_ctx* c, int64_t n, const int32_t* mats, const double* E, int32_t variant,
+                                int32_t iters, double* ms_out, double* checksum)
+{
+    if (!c || !c->have_lib || n < 1 || iters < 1) return fail_arg("emc_bench_lookup: bad arguments");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DBuf<int32_t> dm; DBuf<double> de, dout;
+    if (to_dev(dm, mats, n, st) || to_dev(de, E, n, st) || dout.alloc(n * 17)) return EMC_E_OOM;
+    int grid = c->sm_count * 16;
+    float total = 0;
+    for (int it = 0; it <= iters; ++it) {
+        EMC_TRY_CUDA(cudaEventRecord(c->ev[0], st));
+        switch (variant) {
+        case 1: k_lookup_bench<1><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
+        case 2: k_lookup_bench<2><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
+        case 3: k_lookup_bench<3><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
+        case 4: k_lookup_bench<4><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
+        case 5: k_lookup_bench<5><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
+        case 6: k_lookup_bench<6><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
+        case 7: k_lookup_bench<7><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
+        default: k_lookup_bench<0><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p);
+        }
+        EMC_CHECK_LAUNCH(c);
+        EMC_TRY_CUDA(cudaEventRecord(c->ev[1], st));
+        EMC_TRY_CUDA(cudaEventSynchronize(c->ev[1]));
+        float ms;
+        cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+        if (it > 0) total += ms;   // first launch = warm-up
+    }
+    *ms_out = total / iters;
+    std::vector<double> h(std::min<int64_t>(n, 1024));
+    to_host(h.data(), dout, (int64_t)h.size(), st);
+    EMC_TRY_CUDA(cudaStreamSynchronize(st));
+    double cs = 0;
+    for (double v : h) cs += v;
+    *checksum = cs;
+    dm.release(); de.release(); dout.release();
     return 0;
 }

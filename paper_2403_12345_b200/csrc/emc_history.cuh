@@ -33,12 +33,12 @@ __global__ void __launch_bounds__(128) k_history(BatchP bp, DLib L, DGeom G, DSr
         double dx = p0.b.dx, dy = p0.b.dy, dz = p0.b.dz, E = p0.a.E;
         int kd = p0.d.kind;
         int32_t ax = p0.d.axial, m = p0.d.mat;
-        double* ck = S.ckpt + (int64_t)s * S.nck;
+        double* ck = S.ckpt + s;
         bool fail = false;
         for (;;) {
             // --- lookup (K:573-710)
             double st, sc, sf, snf;
-            macro_tcf(L, m, E, st, sc, sf, snf, bp.fused ? ck : nullptr, S.nck);
+            macro_tcf(L, m, E, st, sc, sf, snf, bp.fused ? ck : nullptr, S.nck, S.nslots);
             interp += 4ull * (unsigned long long)(L.mat_off[m + 1] - L.mat_off[m]);
             nuc_lookups += (unsigned long long)(L.mat_off[m + 1] - L.mat_off[m]);
             ev_l += 1;
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(128) k_history(BatchP bp, DLib L, DGeom G, DSr
                 double u1 = draw(rng, draws);
                 double tgt = __dmul_rn(u1, st);
                 double pt_sel;
-                int32_t ksel = select_nuclide(L, ck, S.nck, e0, e1, bin, E, tgt, bp.fused != 0, pt_sel, interp);
+                int32_t ksel = select_nuclide(L, ck, S.nck, S.nslots, e0, e1, bin, E, tgt, bp.fused != 0, pt_sel, interp);
                 const Comp cs = L.comp[ksel];
                 double s_s, s_c, s_f;
                 micro_scf(L, cs, bin, E, s_s, s_c, s_f);

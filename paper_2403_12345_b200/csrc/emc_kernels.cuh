@@ -97,24 +97,28 @@ __global__ void k_source_init(BatchP bp, DLib L, DGeom G, DSrc src, DSlots S, in
 
 // ----------------------------------------------------------------- sort ---
 
-// Lookup-queue key (composition group, log E, material).  The sort only buys
-// memory coherence for the lookup (physics is sort-invariant, acceptance
-// criterion 1), so the top e_bits of the IEEE pattern (11 exponent +
-// e_bits-11 mantissa bits) suffice and keep the radix sort to 4 passes.
-// Group-major/energy-next puts particles of all fuel segments at similar
-// energy into the same warps (shared records); material is the minor key.
+// Lookup-queue key: (composition group, energy band, material, energy bin).
+// The sort only buys memory coherence for the lookup (physics is
+// sort-invariant, acceptance criterion 1).  Material-uniform warps keep the
+// density gathers uniform; bands (a coarse log-energy partition of the
+// library range) make the whole GPU sweep one band of the grid at a time for
+// all materials of a group, so the record working set stays cache-resident.
+// The fine key is the log-hash bin (~half a grid spacing).
 __global__ void k_sort_keys(const int32_t* __restrict__ q, int32_t n, const PState* __restrict__ ps,
-                            DLib L, uint32_t* __restrict__ keys, int e_bits, int mat_bits, int mat_major)
+                            DLib L, uint32_t* __restrict__ keys, int ebin_bits, int ebin_shift, int mat_bits,
+                            int band_bits, int n_bands)
 {
     int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     int32_t s = q[i];
     const int32_t m = ps[s].d.mat;
-    uint64_t eb = (uint64_t)__double_as_longlong(ps[s].a.E);          // E > 0: monotone bits
-    uint32_t ek = (uint32_t)(eb >> (63 - e_bits)) & ((1u << e_bits) - 1u);
-    uint32_t mk = mat_bits ? ((uint32_t)m & ((1u << mat_bits) - 1u)) : 0u;
-    if (mat_major) keys[i] = (mk << e_bits) | ek;
-    else keys[i] = ((uint32_t)__ldg(L.mat_group + m) << (e_bits + mat_bits)) | (ek << mat_bits) | mk;
+    const uint32_t eb = (uint32_t)energy_bin(ps[s].a.E, L);
+    const uint32_t band = (uint32_t)(((uint64_t)eb * (uint64_t)n_bands) / (uint64_t)L.nbins);
+    uint32_t k = (uint32_t)__ldg(L.mat_group + m);
+    k = (k << band_bits) | band;
+    k = (k << mat_bits) | (uint32_t)m;
+    k = ebin_bits ? ((k << ebin_bits) | (eb >> ebin_shift)) : k;
+    keys[i] = k;
 }
 
 // Permute particle lines into sorted queue order (dst[i] = src[perm[i]]):
@@ -135,11 +139,16 @@ __global__ void __launch_bounds__(256) k_reorder(const int32_t* __restrict__ per
 // its cell material, sequential fold in composition order.  One lane per
 // particle (the fold order is part of the bit-exact contract); the queue is
 // sorted so the 32 lanes of a warp share material and nearby grid brackets.
-#ifndef EMC_LOOKUP_MINB
-#define EMC_LOOKUP_MINB 4
+// One block of NT threads per residency slot: the grid-stride loop hands each
+// block NT *consecutive* queue entries, so with NT = 1024 all 32 warps of an
+// SM work on neighbouring particles (same material, adjacent energies) and
+// share every grid record they gather through L1.
+#ifndef EMC_LOOKUP_PF
+#define EMC_LOOKUP_PF 0
 #endif
-__global__ void __launch_bounds__(256, EMC_LOOKUP_MINB) k_lookup(const int32_t* __restrict__ q, int32_t n, DLib L,
-                                                DSlots S, int32_t fused, unsigned long long* cnt)
+template <int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_lookup(const int32_t* __restrict__ q, int32_t n, DLib L,
+                                                        DSlots S, int32_t fused, unsigned long long* cnt)
 {
     unsigned long long nl = 0;
     EMC_WARP_LOOP(n) {
@@ -149,11 +158,10 @@ __global__ void __launch_bounds__(256, EMC_LOOKUP_MINB) k_lookup(const int32_t* 
             double E = S.ps[s].a.E;
             int32_t m = S.ps[s].d.mat;
             P2 c;
-#if EMC_LOOKUP_ILP > 0
-            macro_tcf_ilp<EMC_LOOKUP_ILP>(L, m, E, c.t, c.c, c.f, c.nsf,
-                                          fused ? S.ckpt + (int64_t)s * S.nck : nullptr, S.nck);
+#if EMC_LOOKUP_PF
+            macro_tcf_pf(L, m, E, c.t, c.c, c.f, c.nsf, fused ? S.ckpt + s : nullptr, S.nck, S.nslots);
 #else
-            macro_tcf(L, m, E, c.t, c.c, c.f, c.nsf, fused ? S.ckpt + (int64_t)s * S.nck : nullptr, S.nck);
+            macro_tcf(L, m, E, c.t, c.c, c.f, c.nsf, fused ? S.ckpt + s : nullptr, S.nck, S.nslots);
 #endif
             S.ps[s].c = c;
             nl += (unsigned long long)(__ldg(L.mat_off + m + 1) - __ldg(L.mat_off + m));
@@ -161,6 +169,68 @@ __global__ void __launch_bounds__(256, EMC_LOOKUP_MINB) k_lookup(const int32_t* 
     }
     warp_add_u64(cnt + CNT_INTERP_TRANSPORT, 4ull * nl);
     warp_add_u64(cnt + CNT_NUCLIDE_LOOKUPS, nl);
+}
+
+// Lookup microbenchmark kernel (tools/lookup_micro.py via emc_bench_lookup):
+// VARIANT 0 = production arithmetic; 1 = no IEEE division (timing ablation);
+// 2 = every lane uses its warp's first energy (perfect record sharing);
+// 3 = no record gathers (synthetic records).  Variants 1-3 compute wrong
+// cross sections on purpose and are never used for transport.
+template <int VARIANT>
+__global__ void __launch_bounds__(256, 4) k_lookup_bench(int32_t n, DLib L, const double* __restrict__ Es,
+                                                         const int32_t* __restrict__ mats, double* __restrict__ out)
+{
+    EMC_WARP_LOOP(n) {
+        int64_t i = emc_base_ + lane_id();
+        double E = i < n ? Es[i] : 1.0;
+        int32_t m = i < n ? mats[i] : 0;
+        if (VARIANT == 2) { E = __shfl_sync(kFull, E, 0); m = __shfl_sync(kFull, m, 0); }
+        if (i < n && VARIANT >= 4) {
+            double st, sc, sf, snf;
+            double* ck = VARIANT == 6 ? nullptr : out + n + i;
+            if (VARIANT == 5) macro_tcf_simple(L, m, E, st, sc, sf, snf, ck, 16, n);
+            else if (VARIANT == 7) macro_tcf_pf(L, m, E, st, sc, sf, snf, ck, 16, n);
+            else macro_tcf(L, m, E, st, sc, sf, snf, ck, 16, n);
+            out[i] = st + sc + sf + snf;
+        } else if (i < n) {
+            const int32_t grp = __ldg(L.mat_group + m);
+            const int32_t e0 = __ldg(L.grp_off + grp), ncomp = __ldg(L.grp_off + grp + 1) - e0;
+            const int32_t bin = energy_bin(E, L);
+            const NucRef* __restrict__ refs = L.gnuc + e0;
+            const DD* __restrict__ dd = L.ddT + m;
+            double st = 0.0, sc = 0.0, sf = 0.0, snf = 0.0;
+            for (int32_t k = 0; k < ncomp; ++k) {
+                const NucRef r = refs[k];
+                const DD w = dd[(int64_t)k * L.n_mat];
+                double t, cc, f;
+                if (VARIANT == 3) {
+                    const double fr = __dmul_rn(E, 1e-9);
+                    t = lerp(1.0 + k, 2.0, fr); cc = lerp(0.5, 1.0 + k, fr); f = lerp(0.1, 0.3, fr);
+                } else {
+                    const int32_t h = __ldg(L.hash + r.hrow + bin);
+                    const Rec* __restrict__ R = L.rec + r.g0;
+                    const int32_t last = r.glen - 1;
+                    int32_t ii = h;
+                    Rec q0 = R[ii], q1 = R[ii + 1];
+                    while (q1.E <= E && ii + 1 < last) { ++ii; q0 = q1; q1 = R[ii + 1]; }
+                    if (ii == 0 && E <= q0.E) { t = q0.t; cc = q0.c; f = q0.f; }
+                    else if (E >= q1.E) { t = q1.t; cc = q1.c; f = q1.f; }
+                    else {
+                        const double fr = VARIANT == 1 ? __dmul_rn(__dsub_rn(E, q0.E), __dsub_rn(q1.E, q0.E))
+                                                       : frac(E, q0.E, q1.E);
+                        t = lerp(q0.t, q1.t, fr);
+                        cc = lerp(q0.c, q1.c, fr);
+                        f = lerp(q0.f, q1.f, fr);
+                    }
+                }
+                st = __dadd_rn(st, __dmul_rn(w.den, t));
+                sc = __dadd_rn(sc, __dmul_rn(w.den, cc));
+                sf = __dadd_rn(sf, __dmul_rn(w.den, f));
+                snf = __dadd_rn(snf, __dmul_rn(w.dn, f));
+            }
+            out[i] = st + sc + sf + snf;
+        }
+    }
 }
 
 // -------------------------------------------------------------- advance ---
@@ -333,7 +403,8 @@ __global__ void __launch_bounds__(256) k_crossing(const int32_t* __restrict__ q,
 // last sigma_t prefix checkpoint <= target written by the lookup, so at most
 // kCkptStride partials are re-interpolated (bit-identical to the stored
 // part_t walk).  Naive: re-interpolate from the first nuclide (K:853-883).
-__device__ __forceinline__ int32_t select_nuclide(const DLib& L, const double* ck, int32_t nck, int32_t e0,
+__device__ __forceinline__ int32_t select_nuclide(const DLib& L, const double* ck, int32_t nck, int64_t cks,
+                                                  int32_t e0,
                                                   int32_t e1, int32_t bin, double E, double tgt,
                                                   bool fused, double& pt_sel, unsigned long long& interp)
 {
@@ -346,10 +417,10 @@ __device__ __forceinline__ int32_t select_nuclide(const DLib& L, const double* c
         int32_t lo = 0, hi = cmax;      // largest c with P_c <= tgt (P_0 = 0)
         while (lo < hi) {
             int32_t mid = (lo + hi + 1) >> 1;
-            if (ck[mid - 1] <= tgt) lo = mid; else hi = mid - 1;
+            if (ck[(int64_t)(mid - 1) * cks] <= tgt) lo = mid; else hi = mid - 1;
         }
         c = lo;
-        if (c > 0) cum = ck[c - 1];
+        if (c > 0) cum = ck[(int64_t)(c - 1) * cks];
     }
     int32_t ksel = e1 - 1;
     pt_sel = 0.0;
@@ -394,7 +465,7 @@ __global__ void __launch_bounds__(256) k_collision(const int32_t* __restrict__ q
             double u1 = draw(b.rng, d.draws);
             double tgt = __dmul_rn(u1, st);
             double pt_sel;
-            int32_t ksel = select_nuclide(L, S.ckpt + (int64_t)s * S.nck, S.nck, e0, e1, bin, E, tgt,
+            int32_t ksel = select_nuclide(L, S.ckpt + s, S.nck, S.nslots, e0, e1, bin, E, tgt,
                                           bp.fused != 0, pt_sel, interp);
             const Comp cs = L.comp[ksel];
             double s_s, s_c, s_f;

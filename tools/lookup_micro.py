@@ -1,0 +1,39 @@
+"""XS-lookup microbenchmark (k_lookup_bench) on the C4 library with a
+realistic in-flight population: 70% fuel (materials 0..99), 30% moderator;
+energies = fission spectrum slowed down by k ~ Poisson(2.6) scatters
+(E' = E*(0.5+0.5u)).  Sorted by (material, E) like the lookup queue.
+
+    python tools/lookup_micro.py [n] [variants...]
+"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2403_12345_b200 as P  # noqa: E402
+from paper_2403_12345_b200 import _native as N  # noqa: E402
+from paper_2403_12345_b200.engine import DeviceEngine  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 8_000_000
+variants = [int(v) for v in sys.argv[2:]] or [0, 1, 2, 3]
+lib, cell = P.depleted_pincell(272, 3, 11303, 100, seed=1)
+eng = DeviceEngine(0)
+eng.upload_library(lib)
+rng = np.random.default_rng(1)
+mats = np.where(rng.random(n) < 0.7, rng.integers(0, 100, n), 100).astype(np.int32)
+E = -1.3e6 * np.log(1 - rng.random(n))
+k = rng.poisson(2.6, n)
+for j in range(k.max()):
+    E = np.where(k > j, E * (0.5 + 0.5 * rng.random(n)), E)
+E = np.clip(E, 1e-5, 2e7)
+order = np.lexsort((E, mats))
+mats, E = np.ascontiguousarray(mats[order]), np.ascontiguousarray(E[order])
+ncomp = np.where(mats < 100, 272, 3)
+nl = int(ncomp.sum())
+for v in variants:
+    ms, cs = C.c_double(), C.c_double()
+    N.check(eng.lib.emc_bench_lookup(eng._h, n, N.ptr(mats), N.ptr(E), v, 5, C.byref(ms), C.byref(cs)), "bench")
+    print(f"variant {v}: {ms.value:8.3f} ms  {nl / ms.value / 1e6:7.1f} G nuclide-lookups/s  "
+          f"{64 * nl / ms.value / 1e6:7.1f} GB/s algorithmic", flush=True)
