@@ -159,9 +159,15 @@ int emc_lcg_skip(emc_ctx *ctx, int64_t n, const uint64_t *state, const uint64_t 
 /* device log/sin/cos replicas (emc_libm.h): out[n][3] */
 int emc_libm_eval(emc_ctx *ctx, int64_t n, const double *x, double *out);
 
+/* division used by the staged lookup (precomputed reciprocal + one FMA
+ * correction) next to the IEEE division: out[2i] = staged n/d, out[2i+1] =
+ * n/d correctly rounded; they must be equal bit for bit (parity test) */
+int emc_div_eval(emc_ctx *ctx, int64_t n, const double *num, const double *den, double *out);
+
 /* tuning harness: mean ms of the XS-lookup microbenchmark kernel over n
  * (material, energy) pairs; variant 0 = production arithmetic, 1-3 = timing
- * ablations (no division / shared energy / no gathers; wrong values) */
+ * ablations (no division / shared energy / no gathers; wrong values), 4-7 =
+ * plain-kernel variants, 8 = the shared-memory-staged production lookup */
 int emc_bench_lookup(emc_ctx *ctx, int64_t n, const int32_t *mats, const double *E, int32_t variant,
                      int32_t iters, double *ms, double *checksum);
 

@@ -82,6 +82,7 @@ SYMBOLS = {
     "emc_replay_bins": (C.c_int, [_P, _I64, _P, _P, _I32, _P]),
     "emc_lcg_skip": (C.c_int, [_P, _I64, _P, _P, _P]),
     "emc_libm_eval": (C.c_int, [_P, _I64, _P, _P]),
+    "emc_div_eval": (C.c_int, [_P, _I64, _P, _P, _P]),
     "emc_launch_count": (_I64, [_P]),
     "emc_bench_lookup": (C.c_int, [_P, _I64, _P, _P, _I32, _I32, C.POINTER(_D), C.POINTER(_D)]),
 }

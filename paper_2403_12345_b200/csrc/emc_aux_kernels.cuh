@@ -159,6 +159,18 @@ __global__ void k_api_libm(int64_t n, const double* __restrict__ x, double* __re
     out[3 * i + 2] = emc_cos(v);
 }
 
+// division check: out[2i] = n/d through the precomputed reciprocal (staged
+// lookup path), out[2i+1] = the IEEE division
+__global__ void k_api_div(int64_t n, const double* __restrict__ num, const double* __restrict__ den,
+                          double* __restrict__ out)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double a = num[i], b = den[i];
+    out[2 * i] = div_by_rcp(a, b, div_rcp(b));
+    out[2 * i + 1] = __ddiv_rn(a, b);
+}
+
 __global__ void k_api_lcg_skip(int64_t n, const uint64_t* __restrict__ s, const uint64_t* __restrict__ k,
                                uint64_t* __restrict__ out)
 {

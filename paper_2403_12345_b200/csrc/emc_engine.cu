@@ -24,6 +24,7 @@
 #include "emc_aux_kernels.cuh"
 #include "emc_history.cuh"
 #include "emc_kernels.cuh"
+#include "emc_lookup_staged.cuh"
 
 using namespace emc;
 
@@ -110,7 +111,7 @@ struct emc_ctx {
     // library
     bool have_lib = false;
     DBuf<Rec> rec; DBuf<double> ch_s, nu; DBuf<int32_t> mat_off; DBuf<Comp> comp; DBuf<int32_t> hash;
-    DBuf<int32_t> mat_group, grp_off; DBuf<NucRef> gnuc; DBuf<DD> ddT;
+    DBuf<int32_t> mat_group, grp_off; DBuf<NucRef> gnuc; DBuf<DD> ddT; DBuf<double> denS; DBuf<IvRec> iv; DBuf<int32_t> nsafe;
     int32_t n_groups = 0;
     DLib L{};
     int32_t n_materials = 0, max_comp = 0;
@@ -135,6 +136,8 @@ struct emc_ctx {
     PState* ps_cur = nullptr;
     bool reorder = true;
     int lookup_block = 1024;
+    bool staged = true;          // k_lookup_staged + energy-major sort (EMC_LOOKUP=plain: k_lookup)
+    size_t lk_smem = 0;
     DSlots S{};
 
     // queues + sort scratch
@@ -203,7 +206,7 @@ extern "C" void emc_destroy(emc_ctx* c)
                     &c->bidx_in, &c->bidx_out, &c->lg_ord, &c->lg_bin})
         b->release();
     c->ps.release(); c->ps2.release(); c->iota.release(); c->rec.release(); c->comp.release();
-    c->mat_group.release(); c->grp_off.release(); c->gnuc.release(); c->ddT.release();
+    c->mat_group.release(); c->grp_off.release(); c->gnuc.release(); c->ddT.release(); c->denS.release(); c->iv.release(); c->nsafe.release();
     c->keys_in.release(); c->keys_out.release(); c->cub_tmp.release();
     c->bkey_in.release(); c->bkey_out.release(); c->lkey_in.release(); c->lkey_out.release();
     c->lg_gid.release(); c->cnt.release(); c->ctl.release();
@@ -310,10 +313,29 @@ extern "C" int emc_upload_library(emc_ctx* c, const emc_library* lib)
     for (int64_t m = 0; m < nm; ++m)
         for (int64_t k = lib->mat_off[m]; k < lib->mat_off[m + 1]; ++k)
             hdd[(size_t)(k - lib->mat_off[m]) * nm + m] = DD{hcomp[k].den, hcomp[k].dn};
+    // staged lookup: densities as [stage][material][LK_G] blocks (one bulk copy per stage)
+    const int64_t nstage = (std::max(maxc, 1) + LK_G - 1) / LK_G;
+    std::vector<double> hden((size_t)nstage * nm * LK_DS, 0.0);
+    for (int64_t m = 0; m < nm; ++m)
+        for (int64_t k = lib->mat_off[m]; k < lib->mat_off[m + 1]; ++k) {
+            const int64_t pos = k - lib->mat_off[m];
+            hden[((size_t)(pos / LK_G) * nm + m) * LK_DS + pos % LK_G] = hcomp[k].den;
+        }
+    const int32_t den_staged = (size_t)LK_D * lk_den_block((int)nm) <= (size_t)LK_DEN_BYTES_MAX;
+    // nuclides whose grid lies where the staged lookup's guard-free division is exact
+    std::vector<int32_t> hsafe(nn, 1);
+    for (int64_t nid = 0; nid < nn; ++nid) {
+        const double* gr = lib->grids + lib->grid_off[nid];
+        const int64_t G = lib->grid_off[nid + 1] - lib->grid_off[nid];
+        for (int64_t i = 0; i < G && hsafe[nid]; ++i) {
+            if (!div_safe_range(gr[i])) hsafe[nid] = 0;
+            if (i + 1 < G && !div_safe_range(gr[i + 1] - gr[i])) hsafe[nid] = 0;
+        }
+    }
 
     int rc = 0;
     rc |= c->mat_group.alloc(nm); rc |= c->grp_off.alloc(hgoff.size()); rc |= c->gnuc.alloc(hgnuc.size());
-    rc |= c->ddT.alloc(hdd.size());
+    rc |= c->ddT.alloc(hdd.size()); rc |= c->denS.alloc(hden.size()); rc |= c->iv.alloc(np); rc |= c->nsafe.alloc(nn);
     rc |= c->rec.alloc(np); rc |= c->ch_s.alloc(np); rc |= c->nu.alloc(nn); rc |= c->mat_off.alloc(nm + 1);
     rc |= c->comp.alloc(hcomp.size()); rc |= c->hash.alloc(hhash.size());
     if (rc) return EMC_E_OOM;
@@ -327,9 +349,31 @@ extern "C" int emc_upload_library(emc_ctx* c, const emc_library* lib)
     EMC_TRY_CUDA(cudaMemcpy(c->grp_off.p, hgoff.data(), hgoff.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     EMC_TRY_CUDA(cudaMemcpy(c->gnuc.p, hgnuc.data(), hgnuc.size() * sizeof(NucRef), cudaMemcpyHostToDevice));
     EMC_TRY_CUDA(cudaMemcpy(c->ddT.p, hdd.data(), hdd.size() * sizeof(DD), cudaMemcpyHostToDevice));
+    EMC_TRY_CUDA(cudaMemcpy(c->denS.p, hden.data(), hden.size() * sizeof(double), cudaMemcpyHostToDevice));
+    EMC_TRY_CUDA(cudaMemcpy(c->nsafe.p, hsafe.data(), nn * sizeof(int32_t), cudaMemcpyHostToDevice));
+    {   // interval records (precomputed differences and reciprocals), built on the device
+        DBuf<int64_t> goff;
+        if (goff.alloc(nn + 1)) return EMC_E_OOM;
+        EMC_TRY_CUDA(cudaMemcpy(goff.p, lib->grid_off, (nn + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+        dim3 grid((unsigned)std::min<int64_t>((gmax + 255) / 256, 64), (unsigned)nn);
+        k_build_intervals<<<grid, 256>>>(c->rec.p, goff.p, (int32_t)nn, c->iv.p);
+        EMC_TRY_CUDA(cudaGetLastError());
+        EMC_TRY_CUDA(cudaDeviceSynchronize());
+        goff.release();
+    }
     c->n_groups = (int32_t)sigs.size();
     c->L = DLib{c->rec.p, c->ch_s.p, c->nu.p, c->mat_off.p, c->comp.p, c->hash.p, key_lo, (int32_t)nbins,
-                shift, lo, hi, c->mat_group.p, c->grp_off.p, c->gnuc.p, c->ddT.p, (int32_t)nm, 0};
+                shift, lo, hi, c->mat_group.p, c->grp_off.p, c->gnuc.p, c->ddT.p, (int32_t)nm, 0,
+                c->iv.p, c->denS.p, den_staged, 0, c->nsafe.p};
+    c->lk_smem = lk_smem_bytes((int)nm, den_staged);
+    EMC_TRY_CUDA(cudaFuncSetAttribute(k_lookup_staged<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)c->lk_smem));
+    EMC_TRY_CUDA(cudaFuncSetAttribute(k_lookup_staged<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)c->lk_smem));
+    EMC_TRY_CUDA(cudaFuncSetAttribute(k_lookup_staged<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)c->lk_smem));
+    EMC_TRY_CUDA(cudaFuncSetAttribute(k_lookup_staged<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)c->lk_smem));
     c->n_materials = (int32_t)nm;
     c->max_comp = maxc;
     c->lib_bytes = (int64_t)(np * (sizeof(Rec) + 8) + hcomp.size() * sizeof(Comp) + hhash.size() * 4);
@@ -385,6 +429,7 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
     int rc = 0;
     rc |= c->ps.alloc(nslots);
     if (const char* lb = getenv("EMC_LOOKUP_BLOCK")) c->lookup_block = atoi(lb);
+    if (const char* lk = getenv("EMC_LOOKUP")) c->staged = std::strcmp(lk, "plain") != 0;
     const char* ro = getenv("EMC_REORDER");
     c->reorder = !(ro && ro[0] == '0');
     if (c->reorder) rc |= c->ps2.alloc(nslots);
@@ -416,6 +461,7 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
         auto bits = [](int64_t v) { int b = 0; while (((int64_t)1 << b) < v) ++b; return b; };
         int nb = 64;
         if (const char* e = getenv("EMC_SORT_BANDS")) nb = std::max(1, atoi(e));
+        if (c->staged) nb = 1;
         c->n_bands = nb;
         c->grp_bits = bits(c->n_groups);
         c->band_bits = bits(nb);
@@ -561,9 +607,14 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             bool do_sort = cf.sort_enabled && nL > 1 && (look_inv % cf.sort_every) == 0;
             EMC_TRY_CUDA(cudaEventRecord(c->ev[0], st));
             if (do_sort) {
-                k_sort_keys<<<grid_for(nL, BLK, 1 << 30), BLK, 0, st>>>(cur, (int32_t)nL, c->ps_cur, c->L,
-                                                                        c->keys_in.p, c->ebin_bits, c->ebin_shift,
-                                                                        c->mat_bits, c->band_bits, c->n_bands);
+                if (c->staged)
+                    k_sort_keys<true><<<grid_for(nL, BLK, 1 << 30), BLK, 0, st>>>(
+                        cur, (int32_t)nL, c->ps_cur, c->L, c->keys_in.p, c->ebin_bits, c->ebin_shift, c->mat_bits,
+                        c->band_bits, c->n_bands);
+                else
+                    k_sort_keys<false><<<grid_for(nL, BLK, 1 << 30), BLK, 0, st>>>(
+                        cur, (int32_t)nL, c->ps_cur, c->L, c->keys_in.p, c->ebin_bits, c->ebin_shift, c->mat_bits,
+                        c->band_bits, c->n_bands);
                 EMC_CHECK_LAUNCH(c);
                 int rc = sort_cub(c, c->keys_in.p, c->keys_out.p, cur, c->qs.p, (int)nL, c->key_bits);
                 if (rc) return rc;
@@ -580,7 +631,15 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             }
             look_inv++;
             EMC_TRY_CUDA(cudaEventRecord(c->ev[1], st));
-            switch (c->lookup_block) {
+            if (c->staged) {
+                const unsigned nb = (unsigned)std::min<int64_t>((nL + LK_CHUNK - 1) / LK_CHUNK, c->sm_count);
+                if (c->L.den_staged)
+                    k_lookup_staged<0, true><<<nb, LK_WARPS * 32, c->lk_smem, st>>>(
+                        q, (int32_t)nL, c->L, c->S, cf.fused, c->cnt.p, nullptr, nullptr, nullptr);
+                else
+                    k_lookup_staged<0, false><<<nb, LK_WARPS * 32, c->lk_smem, st>>>(
+                        q, (int32_t)nL, c->L, c->S, cf.fused, c->cnt.p, nullptr, nullptr, nullptr);
+            } else switch (c->lookup_block) {
             case 1024:
                 k_lookup<1024><<<grid_for(nL, 1024, c->sm_count), 1024, 0, st>>>(q, (int32_t)nL, c->L, c->S,
                                                                                  cf.fused, c->cnt.p);
@@ -973,6 +1032,20 @@ extern "C" int emc_libm_eval(emc_ctx* c, int64_t n, const double* x, double* out
     return 0;
 }
 
+extern "C" int emc_div_eval(emc_ctx* c, int64_t n, const double* num, const double* den, double* out)
+{
+    if (!c) return fail_arg("null ctx");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DBuf<double> dn, dd, dout;
+    if (to_dev(dn, num, n, st) || to_dev(dd, den, n, st) || dout.alloc(std::max<int64_t>(2 * n, 1))) return EMC_E_OOM;
+    if (n) { k_api_div<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(n, dn.p, dd.p, dout.p); EMC_CHECK_LAUNCH(c); }
+    to_host(out, dout, 2 * n, st);
+    EMC_TRY_CUDA(cudaStreamSynchronize(st));
+    dn.release(); dd.release(); dout.release();
+    return 0;
+}
+
 // test/tuning entry point: time k_lookup_bench<variant> over n (mat, E) pairs
 extern "C" int emc_bench_lookup(emc_ctx* c, int64_t n, const int32_t* mats, const double* E, int32_t variant,
                                 int32_t iters, double* ms_out, double* checksum)
@@ -994,6 +1067,16 @@ extern "C" int emc_bench_lookup(emc_ctx* c, int64_t n, const int32_t* mats, cons
         case 5: k_lookup_bench<5><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
         case 6: k_lookup_bench<6><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
         case 7: k_lookup_bench<7><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
+        case 8: {
+            const unsigned nb = (unsigned)std::min<int64_t>((n + LK_CHUNK - 1) / LK_CHUNK, c->sm_count);
+            if (c->L.den_staged)
+                k_lookup_staged<1, true><<<nb, LK_WARPS * 32, c->lk_smem, st>>>(nullptr, (int32_t)n, c->L, c->S, 1,
+                                                                               c->cnt.p, de.p, dm.p, dout.p);
+            else
+                k_lookup_staged<1, false><<<nb, LK_WARPS * 32, c->lk_smem, st>>>(nullptr, (int32_t)n, c->L, c->S,
+                                                                                1, c->cnt.p, de.p, dm.p, dout.p);
+            break;
+        }
         default: k_lookup_bench<0><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p);
         }
         EMC_CHECK_LAUNCH(c);

@@ -104,6 +104,12 @@ __global__ void k_source_init(BatchP bp, DLib L, DGeom G, DSrc src, DSlots S, in
 // library range) make the whole GPU sweep one band of the grid at a time for
 // all materials of a group, so the record working set stays cache-resident.
 // The fine key is the log-hash bin (~half a grid spacing).
+//
+// ENERGY_MAJOR (used with the staged lookup): (group, energy bin, material).
+// A chunk of ~1000 consecutive particles then spans a few grid records per
+// nuclide (the staged windows), and the material key inside a bin makes the
+// shared-memory density reads of a warp mostly broadcasts.
+template <bool ENERGY_MAJOR>
 __global__ void k_sort_keys(const int32_t* __restrict__ q, int32_t n, const PState* __restrict__ ps,
                             DLib L, uint32_t* __restrict__ keys, int ebin_bits, int ebin_shift, int mat_bits,
                             int band_bits, int n_bands)
@@ -113,11 +119,16 @@ __global__ void k_sort_keys(const int32_t* __restrict__ q, int32_t n, const PSta
     int32_t s = q[i];
     const int32_t m = ps[s].d.mat;
     const uint32_t eb = (uint32_t)energy_bin(ps[s].a.E, L);
-    const uint32_t band = (uint32_t)(((uint64_t)eb * (uint64_t)n_bands) / (uint64_t)L.nbins);
     uint32_t k = (uint32_t)__ldg(L.mat_group + m);
-    k = (k << band_bits) | band;
-    k = (k << mat_bits) | (uint32_t)m;
-    k = ebin_bits ? ((k << ebin_bits) | (eb >> ebin_shift)) : k;
+    if (ENERGY_MAJOR) {
+        k = ebin_bits ? ((k << ebin_bits) | (eb >> ebin_shift)) : k;
+        k = (k << mat_bits) | (uint32_t)m;
+    } else {
+        const uint32_t band = (uint32_t)(((uint64_t)eb * (uint64_t)n_bands) / (uint64_t)L.nbins);
+        k = (k << band_bits) | band;
+        k = (k << mat_bits) | (uint32_t)m;
+        k = ebin_bits ? ((k << ebin_bits) | (eb >> ebin_shift)) : k;
+    }
     keys[i] = k;
 }
 
@@ -236,18 +247,25 @@ __global__ void __launch_bounds__(256, 4) k_lookup_bench(int32_t n, DLib L, cons
 // -------------------------------------------------------------- advance ---
 
 // tally scoring of one flight segment into the dense (region, score) bins
-// (fast reduction): warp-aggregated when the warp shares one region.
+// (fast reduction): one warp reduction + atomic per distinct region in the
+// warp for up to three regions (energy-major queues mix a few materials per
+// warp), per-lane atomics for the rest.
 __device__ __forceinline__ void score_bins(double* bins, bool valid, int32_t base, const double v[5])
 {
-    int32_t b0 = __shfl_sync(kFull, valid ? base : -1, __ffs(__ballot_sync(kFull, valid)) - 1);
-    bool uniform = __all_sync(kFull, !valid || base == b0);
-    if (uniform) {
+    unsigned todo = __ballot_sync(kFull, valid);
+    for (int round = 0; round < 3 && todo; ++round) {
+        const int l = __ffs(todo) - 1;
+        const int32_t b = __shfl_sync(kFull, base, l);
+        const bool in = valid && base == b;
+        todo &= ~__ballot_sync(kFull, in);
         #pragma unroll
         for (int k = 0; k < 5; ++k) {
-            double s = warp_sum_f64(valid ? v[k] : 0.0);
-            if (lane_id() == 0 && b0 >= 0 && s != 0.0) atomicAdd(bins + b0 + k, s);
+            double s = warp_sum_f64(in ? v[k] : 0.0);
+            if ((int)lane_id() == l && s != 0.0) atomicAdd(bins + b + k, s);
         }
-    } else if (valid) {
+        if (in) valid = false;
+    }
+    if (valid) {
         #pragma unroll
         for (int k = 0; k < 5; ++k) if (v[k] != 0.0) atomicAdd(bins + base + k, v[k]);
     }

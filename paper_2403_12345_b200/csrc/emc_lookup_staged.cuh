@@ -1,0 +1,373 @@
+// Shared-memory-staged macroscopic cross-section lookup (K:573-710), sm_100a.
+//
+// The lookup queue is sorted by (composition group, log-hash energy bin,
+// material), so the ~1000 particles one CTA takes (a "chunk") share a
+// composition group and span a narrow energy range: for every nuclide of the
+// group, all their brackets lie in a window of a few grid records (2-3 at the
+// C4 population).  One producer warp streams, nuclide by nuclide and LK_D
+// stages ahead, each window plus the row of material densities for that
+// composition position into shared memory with bulk async copies
+// (cp.async.bulk, completion on an mbarrier); 31 consumer warps, one lane per
+// particle, run the reference's sequential fold over the group's nuclides out
+// of shared memory.  The dependent global gathers (hash -> record) of the
+// plain kernel disappear from the per-lane critical path; what is left per
+// (particle, nuclide) is two shared-memory reads and the FP64 arithmetic.
+//
+// Arithmetic, fold order and bracket semantics are exactly macro_tcf's (and
+// thus the reference's): windows only change where a record is read from.
+// Windows wider than LK_R records (sparse populations at the tail of a batch)
+// fall back to the global hash + scan path for that (chunk, nuclide), which is
+// warp-uniform.
+#pragma once
+#include "emc_device.cuh"
+
+namespace emc {
+
+constexpr int LK_WARPS = 32;               // CTA = 31 consumer warps + 1 producer warp
+constexpr int LK_CONS = LK_WARPS - 1;
+constexpr int LK_CHUNK = LK_CONS * 32;     // particles per chunk
+constexpr int LK_G = 8;                    // nuclides per pipeline stage
+constexpr int LK_D = 6;                    // stages in flight
+constexpr int LK_R = 16;                   // staged interval records per nuclide window
+constexpr int LK_SCAN = 4;                 // wider windows start the scan at the hash bound
+constexpr int LK_MIN_NUC = 16;             // smaller groups use the direct path
+constexpr int LK_DS = LK_G + 2;            // doubles per material in a density block (8 used;
+                                           // the 80-byte stride spreads materials over banks)
+constexpr int LK_DEN_BYTES_MAX = 120 * 1024;
+
+enum : int32_t { LK_STAGED = 0, LK_GLOBAL = 1, LK_POINT = 2 };
+
+struct __align__(16) LkMeta {
+    int32_t lo, cnt, last, mode;   // window = interval records [lo, lo+cnt) of the nuclide; last = glen-1
+    double nu;                     // nu of the nuclide (den*nu is formed per lane, K:632 order)
+    int32_t g0, hrow;              // global fallback
+};
+
+struct __align__(128) LkShared {
+    unsigned long long full[LK_D], empty[LK_D];
+    int32_t grp, bmin, bmax, pad;
+    LkMeta meta[LK_D][LK_G];
+    IvRec iv[LK_D][LK_G][LK_R];
+};
+
+// density block of one stage: [n_mat][LK_DS] doubles
+__host__ __device__ constexpr size_t lk_den_block(int n_mat) { return (size_t)n_mat * LK_DS * sizeof(double); }
+
+__host__ __device__ constexpr size_t lk_smem_bytes(int n_mat, int den_staged)
+{
+    return sizeof(LkShared) + (den_staged ? (size_t)LK_D * lk_den_block(n_mat) : 0);
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b)
+{
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_addr(b))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, uint32_t bytes)
+{
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+                     smem_addr(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* b, uint32_t parity)
+{
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_addr(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity)
+{
+    while (!mbar_try_wait(b, parity)) {
+    }
+}
+
+// global -> shared bulk copy (16-byte aligned, size a multiple of 16),
+// completing `bytes` of transaction count on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ int warp_min_i32(int v)
+{
+    for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+__device__ __forceinline__ int warp_max_i32(int v)
+{
+    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Interval records: built once per library upload from the point records.
+__global__ void k_build_intervals(const Rec* __restrict__ rec, const int64_t* __restrict__ grid_off, int32_t n_nuc,
+                                  IvRec* __restrict__ iv)
+{
+    const int32_t nid = blockIdx.y;
+    if (nid >= n_nuc) return;
+    const int64_t a = grid_off[nid], b = grid_off[nid + 1];
+    for (int64_t i = a + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < b; i += (int64_t)gridDim.x * blockDim.x) {
+        const Rec p = rec[i];
+        IvRec v;
+        v.E0 = p.E; v.t0 = p.t; v.c0 = p.c; v.f0 = p.f; v.pad = 0.0;
+        if (i + 1 < b) {
+            const Rec q = rec[i + 1];
+            v.d = __dsub_rn(q.E, p.E);
+            v.r = div_rcp(v.d);
+            v.dt = __dsub_rn(q.t, p.t);
+            v.dc = __dsub_rn(q.c, p.c);
+            v.df = __dsub_rn(q.f, p.f);
+        } else {
+            v.d = 0.0; v.r = 0.0; v.dt = 0.0; v.dc = 0.0; v.df = 0.0;
+        }
+        iv[i] = v;
+    }
+}
+
+// (t, c, f) of one nuclide from global point records (hash + scan): the
+// fallback for windows that did not fit a stage (same values as macro_tcf).
+__device__ __forceinline__ void lk_micro_global(const DLib& L, int32_t g0, int32_t last, int32_t hrow, int32_t bin,
+                                                double E, double& t, double& cc, double& f)
+{
+    const Rec* __restrict__ R = L.rec + g0;
+    int32_t i = __ldg(L.hash + hrow + bin);
+    Rec r0 = R[i], r1 = R[i + 1];
+    while (r1.E <= E && i + 1 < last) { ++i; r0 = r1; r1 = R[i + 1]; }
+    if (i == 0 && E <= r0.E) { t = r0.t; cc = r0.c; f = r0.f; }
+    else if (E >= r1.E) { t = r1.t; cc = r1.c; f = r1.f; }
+    else {
+        const double fr = frac(E, r0.E, r1.E);
+        t = lerp(r0.t, r1.t, fr);
+        cc = lerp(r0.c, r1.c, fr);
+        f = lerp(r0.f, r1.f, fr);
+    }
+}
+
+// One producer lane's view of nuclide k of the current pass.
+struct LkNext {
+    LkMeta mt;
+    bool valid;
+};
+
+__device__ __forceinline__ void lk_prefetch(const DLib& L, int32_t e0, int32_t k, int32_t ncomp, int32_t bmin,
+                                            int32_t bmax, LkNext& nx)
+{
+    nx.valid = k < ncomp;
+    if (!nx.valid) return;
+    const NucRef r = L.gnuc[e0 + k];
+    LkMeta& mt = nx.mt;
+    mt.last = r.glen - 1; mt.g0 = r.g0; mt.hrow = r.hrow; mt.nu = __ldg(L.nu + r.nid);
+    if (mt.last == 0) {
+        mt.mode = LK_POINT; mt.lo = 0; mt.cnt = 1;
+    } else if (!__ldg(L.nsafe + r.nid)) {
+        mt.mode = LK_GLOBAL; mt.lo = 0; mt.cnt = 0;
+    } else {
+        const int32_t lo = __ldg(L.hash + r.hrow + bmin);
+        const int32_t hi = bmax + 1 < L.nbins ? __ldg(L.hash + r.hrow + bmax + 1) : mt.last - 1;
+        mt.lo = lo;
+        mt.cnt = hi - lo + 2;            // intervals lo..hi plus record hi+1 (<= last)
+        mt.mode = mt.cnt <= LK_R ? LK_STAGED : LK_GLOBAL;
+    }
+}
+
+// MODE 0: transport (queue q of slots, writes PState.c and the sigma_t
+//         checkpoints); MODE 1: microbenchmark over (bE, bM), writes
+//         bout[i] = st + sc + sf + snf and checkpoints at bout + n.
+template <int MODE, bool DEN_ST>
+__global__ void __launch_bounds__(LK_WARPS * 32, 1)
+    k_lookup_staged(const int32_t* __restrict__ q, int32_t n, DLib L, DSlots S, int32_t fused,
+                    unsigned long long* cnt, const double* __restrict__ bE, const int32_t* __restrict__ bM,
+                    double* __restrict__ bout)
+{
+    extern __shared__ __align__(128) unsigned char lk_raw[];
+    LkShared& sh = *reinterpret_cast<LkShared*>(lk_raw);
+    double* const sden = reinterpret_cast<double*>(lk_raw + sizeof(LkShared));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool producer = warp == LK_CONS;
+    const int32_t nmat = L.n_mat;
+    const int32_t nck = MODE == 0 ? S.nck : 16;
+
+    if (threadIdx.x == 0) {
+        for (int d = 0; d < LK_D; ++d) {
+            mbar_init(&sh.full[d], 32);
+            mbar_init(&sh.empty[d], LK_CONS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    uint32_t T = 0;                 // pipeline stage counter, identical in every thread
+    unsigned long long nl = 0;
+    for (int64_t base = (int64_t)blockIdx.x * LK_CHUNK; base < n; base += (int64_t)gridDim.x * LK_CHUNK) {
+        const int64_t i = base + threadIdx.x;
+        bool pend = !producer && i < n;
+        int32_t s = 0, m = 0, grp = 0, bin = 0;
+        double E = 1.0;
+        if (pend) {
+            if (MODE == 0) {
+                s = q[i];
+                E = S.ps[s].a.E;
+                m = S.ps[s].d.mat;
+            } else {
+                E = bE[i];
+                m = bM[i];
+            }
+            grp = __ldg(L.mat_group + m);
+            bin = energy_bin(E, L);
+        }
+        // one pass per composition group present in the chunk (normally one)
+        for (;;) {
+            if (threadIdx.x == 0) { sh.grp = INT32_MAX; sh.bmin = INT32_MAX; sh.bmax = -1; }
+            __syncthreads();
+            {
+                const int g = warp_min_i32(pend ? grp : INT32_MAX);
+                if (lane == 0 && g != INT32_MAX) atomicMin(&sh.grp, g);
+            }
+            __syncthreads();
+            const int32_t G = sh.grp;
+            if (G == INT32_MAX) break;
+            const bool mine = pend && grp == G;
+            {
+                const int b0 = warp_min_i32(mine ? bin : INT32_MAX), b1 = warp_max_i32(mine ? bin : -1);
+                if (lane == 0 && b1 >= 0) { atomicMin(&sh.bmin, b0); atomicMax(&sh.bmax, b1); }
+            }
+            __syncthreads();
+            const int32_t bmin = sh.bmin, bmax = sh.bmax;
+            const int32_t e0 = __ldg(L.grp_off + G), ncomp = __ldg(L.grp_off + G + 1) - e0;
+            double st = 0.0, sc = 0.0, sf = 0.0, snf = 0.0;
+            double* ck = nullptr;
+            int64_t cks = 1;
+            if (MODE == 0) { if (fused) { ck = S.ckpt + s; cks = S.nslots; } }
+            else { ck = bout + n + i; cks = n; }
+            const int nst = (ncomp + LK_G - 1) / LK_G;
+
+            if (ncomp < LK_MIN_NUC) {
+                if (mine) macro_tcf(L, m, E, st, sc, sf, snf, ck, nck, cks);
+            } else if (producer) {
+                // lane j < LK_G owns nuclide 8t+j of every stage; its global
+                // reads for stage t+1 are issued before it waits for slot t
+                LkNext nx;
+                nx.valid = false;
+                if (lane < LK_G) lk_prefetch(L, e0, lane, ncomp, bmin, bmax, nx);
+                for (int t = 0; t < nst; ++t, ++T) {
+                    const int d = (int)(T % LK_D);
+                    const LkNext cur = nx;
+                    if (lane < LK_G && t + 1 < nst) lk_prefetch(L, e0, (t + 1) * LK_G + lane, ncomp, bmin, bmax, nx);
+                    if (T >= (uint32_t)LK_D) mbar_wait(&sh.empty[d], ((T / LK_D) - 1) & 1);
+                    uint32_t bytes = 0;
+                    const bool copy_iv = lane < LK_G && cur.valid && cur.mt.mode != LK_GLOBAL;
+                    if (lane < LK_G && cur.valid) sh.meta[d][lane] = cur.mt;
+                    if (copy_iv) bytes += (uint32_t)cur.mt.cnt * (uint32_t)sizeof(IvRec);
+                    if (DEN_ST && lane == 0) bytes += (uint32_t)lk_den_block(nmat);
+                    // expect before issuing so the phase cannot complete early
+                    mbar_arrive_tx(&sh.full[d], bytes);
+                    if (copy_iv)
+                        bulk_g2s(&sh.iv[d][lane][0], L.iv + cur.mt.g0 + cur.mt.lo,
+                                 (uint32_t)cur.mt.cnt * (uint32_t)sizeof(IvRec), &sh.full[d]);
+                    if (DEN_ST && lane == 0)
+                        bulk_g2s(sden + (size_t)d * nmat * LK_DS, L.denS + (size_t)t * nmat * LK_DS,
+                                 (uint32_t)lk_den_block(nmat), &sh.full[d]);
+                }
+            } else {
+                for (int t = 0; t < nst; ++t, ++T) {
+                    const int d = (int)(T % LK_D);
+                    mbar_wait(&sh.full[d], (T / LK_D) & 1);
+                    if (mine) {
+                        const double* dens = DEN_ST ? sden + ((size_t)d * nmat + m) * LK_DS : nullptr;
+#pragma unroll
+                        for (int j = 0; j < LK_G; ++j) {
+                            const int k = t * LK_G + j;
+                            if (k >= ncomp) break;
+                            const LkMeta& mt = sh.meta[d][j];
+                            const double den = DEN_ST ? dens[j] : L.ddT[(int64_t)k * nmat + m].den;
+                            const int4 mi = *reinterpret_cast<const int4*>(&mt);   // lo, cnt, last, mode
+                            double tt, cc, ff;
+                            if (__builtin_expect(mi.w == LK_STAGED, 1)) {
+                                const IvRec* W = sh.iv[d][j];
+                                int32_t li;
+                                if (mi.y <= 4) {
+                                    // <= 3 intervals: li = #{j in 1..cnt-2 : E0_j <= E} (grids ascend)
+                                    const double a1 = W[1].E0, a2 = W[2].E0;
+                                    li = (int32_t)(mi.y >= 3 && a1 <= E) + (int32_t)(mi.y >= 4 && a2 <= E);
+                                } else {
+                                    const int32_t lim = mi.z - mi.x;
+                                    li = __ldg(L.hash + mt.hrow + bin) - mi.x;
+                                    while (li + 1 < lim && W[li + 1].E0 <= E) ++li;
+                                }
+                                const IvRec& a = W[li];
+                                const double e0v = a.E0, e1 = W[li + 1].E0;
+                                if (__builtin_expect((mi.x + li == 0 && E <= e0v) || E >= e1, 0)) {
+                                    const IvRec& b = E >= e1 && !(mi.x + li == 0 && E <= e0v) ? W[li + 1] : a;
+                                    tt = b.t0; cc = b.c0; ff = b.f0;
+                                } else {
+                                    const double fr = div_by_rcp_safe(__dsub_rn(E, e0v), a.d, a.r);
+                                    tt = __dadd_rn(a.t0, __dmul_rn(fr, a.dt));
+                                    cc = __dadd_rn(a.c0, __dmul_rn(fr, a.dc));
+                                    ff = __dadd_rn(a.f0, __dmul_rn(fr, a.df));
+                                }
+                            } else if (mi.w == LK_POINT) {
+                                const IvRec& a = sh.iv[d][j][0];
+                                tt = a.t0; cc = a.c0; ff = a.f0;
+                            } else {
+                                lk_micro_global(L, mt.g0, mi.z, mt.hrow, bin, E, tt, cc, ff);
+                            }
+                            const double dn = __dmul_rn(den, mt.nu);
+                            st = __dadd_rn(st, __dmul_rn(den, tt));
+                            sc = __dadd_rn(sc, __dmul_rn(den, cc));
+                            sf = __dadd_rn(sf, __dmul_rn(den, ff));
+                            snf = __dadd_rn(snf, __dmul_rn(dn, ff));
+                        }
+                        // prefix checkpoint after every kCkptStride (= 2 stages) nuclides
+                        static_assert(kCkptStride == 2 * LK_G, "checkpoint every second stage");
+                        if (ck && (t & 1) && (t + 1) * LK_G <= ncomp) {
+                            const int32_t row = t >> 1;
+                            if (row < nck) ck[(int64_t)row * cks] = st;
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&sh.empty[d]);
+                }
+            }
+            if (mine) {
+                if (MODE == 0) {
+                    P2 c; c.t = st; c.c = sc; c.f = sf; c.nsf = snf;
+                    S.ps[s].c = c;
+                } else {
+                    bout[i] = st + sc + sf + snf;
+                }
+                nl += (unsigned long long)ncomp;
+                pend = false;
+            }
+            __syncthreads();
+        }
+    }
+    if (MODE == 0 && !producer) {
+        warp_add_u64(cnt + CNT_INTERP_TRANSPORT, 4ull * nl);
+        warp_add_u64(cnt + CNT_NUCLIDE_LOOKUPS, nl);
+    }
+}
+
+}  // namespace emc

@@ -217,6 +217,14 @@ class DeviceEngine:
         N.check(self.lib.emc_libm_eval(self._h, x.shape[0], N.ptr(x), N.ptr(out)), "emc_libm_eval")
         return out
 
+    def div(self, num: np.ndarray, den: np.ndarray) -> np.ndarray:
+        """[n, 2]: staged-lookup division (precomputed reciprocal) and IEEE n/d."""
+        num = np.ascontiguousarray(num, np.float64)
+        den = np.ascontiguousarray(den, np.float64)
+        out = np.zeros((num.shape[0], 2))
+        N.check(self.lib.emc_div_eval(self._h, num.shape[0], N.ptr(num), N.ptr(den), N.ptr(out)), "emc_div_eval")
+        return out
+
 
 _API: DeviceEngine | None = None
 

@@ -28,7 +28,8 @@ def _config(run):
 
 
 RUNS = ["small_history", "small_event_cap16", "small_event_naive", "small_perturb17",
-        "small_seed6", "small_inact0", "small_hotsrc", "analytic_event_w2", "c1_event"]
+        "small_seed6", "small_inact0", "small_hotsrc", "analytic_event_w2", "c1_event",
+        "preset251_event_w2"]
 
 
 @pytest.mark.parametrize("name", RUNS)
@@ -199,3 +200,55 @@ def test_oracle_agrees_on_fresh_problem():
     ores = driver.run(dict(cfg.__dict__), lib.arrays(), cell.as_tuple())
     assert res.physics_fingerprint() == driver.fingerprint(ores)
     assert res.counters["events_lookup"] == ores["counters"]["events_lookup"]
+
+
+def _run_with_lookup(kernel, cfg, lib, cell):
+    old = os.environ.get("EMC_LOOKUP")
+    os.environ["EMC_LOOKUP"] = kernel
+    try:
+        return P.run_replicated(cfg, lib, cell)
+    finally:
+        if old is None:
+            os.environ.pop("EMC_LOOKUP", None)
+        else:
+            os.environ["EMC_LOOKUP"] = old
+
+
+@pytest.mark.parametrize("ppb", [1_000_000, 4_000_000])
+def test_staged_lookup_equals_plain_c4(ppb):
+    """The shared-memory-staged lookup (production) against the plain gather
+    kernel on the C4 library at populations where the staged windows carry the
+    lookup: histories, k series, banks and counters must be identical."""
+    lib, cell = P.depleted_pincell(272, 3, 11303, 100, seed=1)
+    cfg = P.RunConfig(particles_per_batch=ppb, inactive_batches=1, active_batches=2, mode="event",
+                      seed=42, max_in_flight=ppb, reduction="deterministic")
+    a = _run_with_lookup("staged", cfg, lib, cell)
+    b = _run_with_lookup("plain", cfg, lib, cell)
+    assert np.array_equal(a.keff.values, b.keff.values)
+    assert np.array_equal(a.batch_sums, b.batch_sums)
+    assert a.physics_fingerprint() == b.physics_fingerprint()
+    assert a.counters["interp_transport"] == b.counters["interp_transport"]
+
+
+def test_staged_division_is_ieee():
+    """The staged lookup divides by a precomputed reciprocal plus one FMA
+    correction; it must equal the IEEE division bit for bit on every grid
+    interval of the C4 library (random position inside the interval, the
+    interval ends, tiny offsets) and on random operands."""
+    from paper_2403_12345_b200.engine import api_engine
+    lib, _ = P.depleted_pincell(272, 3, 11303, 100, seed=1)
+    grid_off, grids = lib.arrays()[0], lib.arrays()[1]
+    last = np.zeros(grids.shape[0], bool)
+    last[grid_off[1:] - 1] = True
+    e0, e1 = grids[:-1][~last[:-1]], grids[1:][~last[:-1]]
+    d = e1 - e0
+    rng = np.random.default_rng(11)
+    nums = [rng.random(d.shape[0]) * d, np.zeros_like(d), d, np.nextafter(d, 0), d * 1e-300,
+            np.full_like(d, 5e-324), (rng.random(d.shape[0]) * 2**-40) * d]
+    num = np.concatenate(nums)
+    den = np.tile(d, len(nums))
+    a = rng.random(4_000_000) * 10.0 ** rng.integers(-30, 30, 4_000_000)
+    b = rng.random(4_000_000) * 10.0 ** rng.integers(-30, 30, 4_000_000)
+    out = api_engine().div(np.concatenate([num, a]), np.concatenate([den, b]))
+    assert np.array_equal(out[:, 0].view(np.uint64), out[:, 1].view(np.uint64))
+    assert np.array_equal(out[:, 1], np.concatenate([num, a]) / np.concatenate([den, b]))

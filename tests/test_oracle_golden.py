@@ -121,3 +121,10 @@ def test_oracle_error_codes(golden):
         driver.run(dict(particles_per_batch=1, inactive_batches=0, active_batches=1, mode="history",
                         seed=1), arrays, geom)
     assert e.value.kind == golden["errors"]["runaway_log"]
+
+
+def test_preset251_library_fixture_matches_reference(golden):
+    from conftest import golden_library
+    import paper_2403_12345_b200 as P
+    lib = golden_library("preset251")
+    assert P.xslib.library_fingerprint(lib) == golden["problems"]["preset251"]["library_fingerprint"]
