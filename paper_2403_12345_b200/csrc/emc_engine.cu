@@ -138,6 +138,7 @@ struct emc_ctx {
     int lookup_block = 1024;
     bool staged = true;          // k_lookup_staged + energy-major sort (EMC_LOOKUP=plain: k_lookup)
     size_t lk_smem = 0;
+    int lk_cfg = 0;              // staged-lookup launch configuration (EMC_LK_CFG)
     DSlots S{};
 
     // queues + sort scratch
@@ -319,7 +320,9 @@ extern "C" int emc_upload_library(emc_ctx* c, const emc_library* lib)
     for (int64_t m = 0; m < nm; ++m)
         for (int64_t k = lib->mat_off[m]; k < lib->mat_off[m + 1]; ++k) {
             const int64_t pos = k - lib->mat_off[m];
-            hden[((size_t)(pos / LK_G) * nm + m) * LK_DS + pos % LK_G] = hcomp[k].den;
+            double* e = &hden[((size_t)(pos / LK_G) * nm + m) * LK_DS + 2 * (pos % LK_G)];
+            e[0] = hcomp[k].den;
+            e[1] = hcomp[k].dn;      // den*nu exactly as the reference forms it (K:632)
         }
     const int32_t den_staged = (size_t)LK_D * lk_den_block((int)nm) <= (size_t)LK_DEN_BYTES_MAX;
     // nuclides whose grid lies where the staged lookup's guard-free division is exact
@@ -366,14 +369,8 @@ extern "C" int emc_upload_library(emc_ctx* c, const emc_library* lib)
                 shift, lo, hi, c->mat_group.p, c->grp_off.p, c->gnuc.p, c->ddT.p, (int32_t)nm, 0,
                 c->iv.p, c->denS.p, den_staged, 0, c->nsafe.p};
     c->lk_smem = lk_smem_bytes((int)nm, den_staged);
-    EMC_TRY_CUDA(cudaFuncSetAttribute(k_lookup_staged<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)c->lk_smem));
-    EMC_TRY_CUDA(cudaFuncSetAttribute(k_lookup_staged<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)c->lk_smem));
-    EMC_TRY_CUDA(cudaFuncSetAttribute(k_lookup_staged<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)c->lk_smem));
-    EMC_TRY_CUDA(cudaFuncSetAttribute(k_lookup_staged<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)c->lk_smem));
+    EMC_TRY_CUDA(lk_set_smem(c->lk_smem));
+    if (const char* lc = getenv("EMC_LK_CFG")) c->lk_cfg = std::max(0, std::min(LK_NCFG - 1, atoi(lc)));
     c->n_materials = (int32_t)nm;
     c->max_comp = maxc;
     c->lib_bytes = (int64_t)(np * (sizeof(Rec) + 8) + hcomp.size() * sizeof(Comp) + hhash.size() * 4);
@@ -465,6 +462,10 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
         c->n_bands = nb;
         c->grp_bits = bits(c->n_groups);
         c->band_bits = bits(nb);
+        if (c->staged) {     // energy-major key: band field = fine energy bits (EMC_SORT_FINE)
+            c->band_bits = 5;
+            if (const char* e = getenv("EMC_SORT_FINE")) c->band_bits = std::max(0, std::min(12, atoi(e)));
+        }
         c->mat_bits = bits(c->n_materials);
         c->ebin_bits = bits(c->L.nbins);
         int total = c->grp_bits + c->band_bits + c->mat_bits + c->ebin_bits;
@@ -632,13 +633,8 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             look_inv++;
             EMC_TRY_CUDA(cudaEventRecord(c->ev[1], st));
             if (c->staged) {
-                const unsigned nb = (unsigned)std::min<int64_t>((nL + LK_CHUNK - 1) / LK_CHUNK, c->sm_count);
-                if (c->L.den_staged)
-                    k_lookup_staged<0, true><<<nb, LK_WARPS * 32, c->lk_smem, st>>>(
-                        q, (int32_t)nL, c->L, c->S, cf.fused, c->cnt.p, nullptr, nullptr, nullptr);
-                else
-                    k_lookup_staged<0, false><<<nb, LK_WARPS * 32, c->lk_smem, st>>>(
-                        q, (int32_t)nL, c->L, c->S, cf.fused, c->cnt.p, nullptr, nullptr, nullptr);
+                EMC_TRY_CUDA(lk_launch<0>(c->lk_cfg, c->L, q, nL, c->S, cf.fused, c->cnt.p, nullptr, nullptr, nullptr,
+                                          c->sm_count, c->lk_smem, st));
             } else switch (c->lookup_block) {
             case 1024:
                 k_lookup<1024><<<grid_for(nL, 1024, c->sm_count), 1024, 0, st>>>(q, (int32_t)nL, c->L, c->S,
@@ -1068,13 +1064,8 @@ extern "C" int emc_bench_lookup(emc_ctx* c, int64_t n, const int32_t* mats, cons
         case 6: k_lookup_bench<6><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
         case 7: k_lookup_bench<7><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
         case 8: {
-            const unsigned nb = (unsigned)std::min<int64_t>((n + LK_CHUNK - 1) / LK_CHUNK, c->sm_count);
-            if (c->L.den_staged)
-                k_lookup_staged<1, true><<<nb, LK_WARPS * 32, c->lk_smem, st>>>(nullptr, (int32_t)n, c->L, c->S, 1,
-                                                                               c->cnt.p, de.p, dm.p, dout.p);
-            else
-                k_lookup_staged<1, false><<<nb, LK_WARPS * 32, c->lk_smem, st>>>(nullptr, (int32_t)n, c->L, c->S,
-                                                                                1, c->cnt.p, de.p, dm.p, dout.p);
+            EMC_TRY_CUDA(lk_launch<1>(c->lk_cfg, c->L, nullptr, n, c->S, 1, c->cnt.p, de.p, dm.p, dout.p, c->sm_count,
+                                      c->lk_smem, st));
             break;
         }
         default: k_lookup_bench<0><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p);

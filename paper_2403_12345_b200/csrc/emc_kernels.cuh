@@ -14,6 +14,16 @@
 
 namespace emc {
 
+// Minimum resident 256-thread blocks per SM for the event kernels: bounds
+// their registers so enough warps are resident to hide the gather latency
+// (measured: collision 80 -> 63 ms per C4 batch at 4 blocks/SM).
+#ifndef EMC_ADV_MINB
+#define EMC_ADV_MINB 3
+#endif
+#ifndef EMC_COL_MINB
+#define EMC_COL_MINB 4
+#endif
+
 // Warp-uniform grid-stride loop: every lane of a warp runs the same number of
 // iterations (warp-synchronous helpers need all 32 lanes); `valid` masks the
 // tail.
@@ -121,8 +131,14 @@ __global__ void k_sort_keys(const int32_t* __restrict__ q, int32_t n, const PSta
     const uint32_t eb = (uint32_t)energy_bin(ps[s].a.E, L);
     uint32_t k = (uint32_t)__ldg(L.mat_group + m);
     if (ENERGY_MAJOR) {
+        // band_bits = extra energy bits below the hash bin (warps of one
+        // material then span a fraction of the bin: more broadcast reads)
         k = ebin_bits ? ((k << ebin_bits) | (eb >> ebin_shift)) : k;
         k = (k << mat_bits) | (uint32_t)m;
+        if (band_bits) {
+            const uint64_t eb64 = (uint64_t)__double_as_longlong(ps[s].a.E);
+            k = (k << band_bits) | (uint32_t)((eb64 >> (L.shift - band_bits)) & ((1u << band_bits) - 1u));
+        }
     } else {
         const uint32_t band = (uint32_t)(((uint64_t)eb * (uint64_t)n_bands) / (uint64_t)L.nbins);
         k = (k << band_bits) | band;
@@ -273,7 +289,7 @@ __device__ __forceinline__ void score_bins(double* bins, bool valid, int32_t bas
 
 // K:713-811 (first half): sample the flight distance, score the segment,
 // move.  Collisions go to q_col, surface hits to q_cross.
-__global__ void __launch_bounds__(256) k_advance(const int32_t* __restrict__ q, int32_t n, BatchP bp,
+__global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __restrict__ q, int32_t n, BatchP bp,
                                                  DLib L, DGeom G, DSlots S, DLog lg, double* bins,
                                                  int32_t* q_col, int32_t* q_cross, Ctl* ctl,
                                                  unsigned long long* cnt)
@@ -381,7 +397,7 @@ __global__ void __launch_bounds__(256) k_advance(const int32_t* __restrict__ q, 
 
 // K:782-811 (second half of the reference advance): reflect on the outer
 // box planes, nudge past the surface, update cell and material.
-__global__ void __launch_bounds__(256) k_crossing(const int32_t* __restrict__ q, const unsigned int* nq,
+__global__ void __launch_bounds__(256, EMC_COL_MINB) k_crossing(const int32_t* __restrict__ q, const unsigned int* nq,
                                                   DGeom G, DSlots S, int32_t* q_next, Ctl* ctl)
 {
     const int32_t n = (int32_t)*nq;
@@ -442,19 +458,54 @@ __device__ __forceinline__ int32_t select_nuclide(const DLib& L, const double* c
     }
     int32_t ksel = e1 - 1;
     pt_sel = 0.0;
-    for (int32_t k = e0 + c * kCkptStride; k < e1; ++k) {
-        const Comp cc = L.comp[k];
-        double pt = __dmul_rn(cc.den, micro_t(L, cc, bin, E));
-        if (!fused) interp += 1;
-        pt_sel = pt;
-        if (__dadd_rn(cum, pt) > tgt) { ksel = k; break; }
-        cum = __dadd_rn(cum, pt);
+    // walk in groups of SN nuclides: the composition, hash and record reads
+    // of a group are independent and issued together; the comparison walk
+    // over the group stays sequential (same cum and pt values as K:846-852)
+#ifndef EMC_WALK_SN
+#define EMC_WALK_SN 2
+#endif
+    constexpr int SN = EMC_WALK_SN;
+    for (int32_t k0 = e0 + c * kCkptStride; k0 < e1; k0 += SN) {
+        double den[SN], e0v[SN], t0[SN], e1v[SN], t1[SN];
+        int32_t st[SN];
+        #pragma unroll
+        for (int u = 0; u < SN; ++u) {
+            const int32_t k = min(k0 + u, e1 - 1);
+            const Comp cc = L.comp[k];
+            den[u] = cc.den;
+            const Rec* __restrict__ R = L.rec + cc.g0;
+            const int32_t last = cc.glen - 1;
+            int32_t i = last > 0 ? __ldg(L.hash + (int64_t)cc.nid * L.nbins + bin) : 0;
+            const double2 p0 = *reinterpret_cast<const double2*>(&R[i].E);        // (E, t) of point i
+            const double2 p1 = *reinterpret_cast<const double2*>(&R[min(i + 1, last)].E);
+            e0v[u] = p0.x; t0[u] = p0.y; e1v[u] = p1.x; t1[u] = p1.y;
+            if (last == 0) { st[u] = 1; continue; }
+            if (e1v[u] <= E && i + 1 < last) {     // rare: bracket beyond the hashed lower bound
+                do {
+                    ++i; e0v[u] = e1v[u]; t0[u] = t1[u];
+                    const double2 q = *reinterpret_cast<const double2*>(&R[i + 1].E);
+                    e1v[u] = q.x; t1[u] = q.y;
+                } while (e1v[u] <= E && i + 1 < last);
+            }
+            st[u] = (i == 0 && E <= e0v[u]) ? 1 : (E >= e1v[u] ? 2 : 0);
+        }
+        #pragma unroll
+        for (int u = 0; u < SN; ++u) {
+            const int32_t k = k0 + u;
+            if (k >= e1) break;
+            const double mt = st[u] == 1 ? t0[u] : st[u] == 2 ? t1[u] : lerp(t0[u], t1[u], frac(E, e0v[u], e1v[u]));
+            double pt = __dmul_rn(den[u], mt);
+            if (!fused) interp += 1;
+            pt_sel = pt;
+            if (__dadd_rn(cum, pt) > tgt) { return k; }
+            cum = __dadd_rn(cum, pt);
+        }
     }
     return ksel;
 }
 
 // K:814-923 + refill (K:1187-1202)
-__global__ void __launch_bounds__(256) k_collision(const int32_t* __restrict__ q, const unsigned int* nq,
+__global__ void __launch_bounds__(256, EMC_COL_MINB) k_collision(const int32_t* __restrict__ q, const unsigned int* nq,
                                                    BatchP bp, DLib L, DGeom G, DSrc src, DSlots S,
                                                    DLog lg, DSites sb, double* bins, int32_t* q_next,
                                                    Ctl* ctl, unsigned long long* cnt)

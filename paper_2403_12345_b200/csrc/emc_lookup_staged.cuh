@@ -19,21 +19,21 @@
 // fall back to the global hash + scan path for that (chunk, nuclide), which is
 // warp-uniform.
 #pragma once
+#include <algorithm>
 #include "emc_device.cuh"
 
 namespace emc {
 
-constexpr int LK_WARPS = 32;               // CTA = 31 consumer warps + 1 producer warp
-constexpr int LK_CONS = LK_WARPS - 1;
-constexpr int LK_CHUNK = LK_CONS * 32;     // particles per chunk
+// CTA = NW warps: NW-1 consumer warps (one particle per lane; a chunk is
+// (NW-1)*32 consecutive queue entries) + 1 producer warp; MINB CTAs per SM.
 constexpr int LK_G = 8;                    // nuclides per pipeline stage
 constexpr int LK_D = 6;                    // stages in flight
 constexpr int LK_R = 16;                   // staged interval records per nuclide window
 constexpr int LK_SCAN = 4;                 // wider windows start the scan at the hash bound
 constexpr int LK_MIN_NUC = 16;             // smaller groups use the direct path
-constexpr int LK_DS = LK_G + 2;            // doubles per material in a density block (8 used;
-                                           // the 80-byte stride spreads materials over banks)
-constexpr int LK_DEN_BYTES_MAX = 120 * 1024;
+constexpr int LK_DS = 2 * LK_G + 2;        // doubles per material in a density block: 8 (den, den*nu)
+                                           // pairs; the 144-byte stride spreads materials over banks
+constexpr int LK_DEN_BYTES_MAX = 150 * 1024;
 
 enum : int32_t { LK_STAGED = 0, LK_GLOBAL = 1, LK_POINT = 2 };
 
@@ -166,6 +166,13 @@ __device__ __forceinline__ void lk_micro_global(const DLib& L, int32_t g0, int32
     }
 }
 
+// a <= b for positive doubles (energies): integer compare of the bit patterns
+// keeps the bracket tests off the FP64 pipe
+__device__ __forceinline__ bool pos_le(double a, double b)
+{
+    return __double_as_longlong(a) <= __double_as_longlong(b);
+}
+
 // One producer lane's view of nuclide k of the current pass.
 struct LkNext {
     LkMeta mt;
@@ -196,8 +203,8 @@ __device__ __forceinline__ void lk_prefetch(const DLib& L, int32_t e0, int32_t k
 // MODE 0: transport (queue q of slots, writes PState.c and the sigma_t
 //         checkpoints); MODE 1: microbenchmark over (bE, bM), writes
 //         bout[i] = st + sc + sf + snf and checkpoints at bout + n.
-template <int MODE, bool DEN_ST>
-__global__ void __launch_bounds__(LK_WARPS * 32, 1)
+template <int MODE, bool DEN_ST, int NW, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
     k_lookup_staged(const int32_t* __restrict__ q, int32_t n, DLib L, DSlots S, int32_t fused,
                     unsigned long long* cnt, const double* __restrict__ bE, const int32_t* __restrict__ bM,
                     double* __restrict__ bout)
@@ -206,6 +213,7 @@ __global__ void __launch_bounds__(LK_WARPS * 32, 1)
     LkShared& sh = *reinterpret_cast<LkShared*>(lk_raw);
     double* const sden = reinterpret_cast<double*>(lk_raw + sizeof(LkShared));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int LK_CONS = NW - 1, LK_CHUNK = LK_CONS * 32;
     const bool producer = warp == LK_CONS;
     const int32_t nmat = L.n_mat;
     const int32_t nck = MODE == 0 ? S.nck : 16;
@@ -302,16 +310,19 @@ __global__ void __launch_bounds__(LK_WARPS * 32, 1)
                             const int k = t * LK_G + j;
                             if (k >= ncomp) break;
                             const LkMeta& mt = sh.meta[d][j];
-                            const double den = DEN_ST ? dens[j] : L.ddT[(int64_t)k * nmat + m].den;
+                            const double2 dd = DEN_ST ? *reinterpret_cast<const double2*>(dens + 2 * j)
+                                                      : *reinterpret_cast<const double2*>(&L.ddT[(int64_t)k * nmat + m]);
+                            const double den = dd.x, dn = dd.y;
                             const int4 mi = *reinterpret_cast<const int4*>(&mt);   // lo, cnt, last, mode
+                            const IvRec* W = sh.iv[d][j];
+                            // issued together with the meta read (always in-bounds shared memory)
+                            const double a1 = W[1].E0, a2 = W[2].E0;
                             double tt, cc, ff;
                             if (__builtin_expect(mi.w == LK_STAGED, 1)) {
-                                const IvRec* W = sh.iv[d][j];
                                 int32_t li;
                                 if (mi.y <= 4) {
                                     // <= 3 intervals: li = #{j in 1..cnt-2 : E0_j <= E} (grids ascend)
-                                    const double a1 = W[1].E0, a2 = W[2].E0;
-                                    li = (int32_t)(mi.y >= 3 && a1 <= E) + (int32_t)(mi.y >= 4 && a2 <= E);
+                                    li = (int32_t)(mi.y >= 3 && pos_le(a1, E)) + (int32_t)(mi.y >= 4 && pos_le(a2, E));
                                 } else {
                                     const int32_t lim = mi.z - mi.x;
                                     li = __ldg(L.hash + mt.hrow + bin) - mi.x;
@@ -319,8 +330,9 @@ __global__ void __launch_bounds__(LK_WARPS * 32, 1)
                                 }
                                 const IvRec& a = W[li];
                                 const double e0v = a.E0, e1 = W[li + 1].E0;
-                                if (__builtin_expect((mi.x + li == 0 && E <= e0v) || E >= e1, 0)) {
-                                    const IvRec& b = E >= e1 && !(mi.x + li == 0 && E <= e0v) ? W[li + 1] : a;
+                                const bool lo_clamp = mi.x + li == 0 && pos_le(E, e0v), hi_clamp = pos_le(e1, E);
+                                if (__builtin_expect(lo_clamp || hi_clamp, 0)) {
+                                    const IvRec& b = hi_clamp && !lo_clamp ? W[li + 1] : a;
                                     tt = b.t0; cc = b.c0; ff = b.f0;
                                 } else {
                                     const double fr = div_by_rcp_safe(__dsub_rn(E, e0v), a.d, a.r);
@@ -334,7 +346,6 @@ __global__ void __launch_bounds__(LK_WARPS * 32, 1)
                             } else {
                                 lk_micro_global(L, mt.g0, mi.z, mt.hrow, bin, E, tt, cc, ff);
                             }
-                            const double dn = __dmul_rn(den, mt.nu);
                             st = __dadd_rn(st, __dmul_rn(den, tt));
                             sc = __dadd_rn(sc, __dmul_rn(den, cc));
                             sf = __dadd_rn(sf, __dmul_rn(den, ff));
@@ -368,6 +379,63 @@ __global__ void __launch_bounds__(LK_WARPS * 32, 1)
         warp_add_u64(cnt + CNT_INTERP_TRANSPORT, 4ull * nl);
         warp_add_u64(cnt + CNT_NUCLIDE_LOOKUPS, nl);
     }
+}
+
+}  // namespace emc
+
+namespace emc {
+
+// Launch configurations of the staged lookup (warps per CTA x CTAs per SM).
+// EMC_LK_CFG selects one at run time (tuning); 0 is the default.
+constexpr int LK_NCFG = 3;
+constexpr int lk_cfg_warps(int c) { return c == 1 ? 20 : c == 2 ? 16 : 32; }
+constexpr int lk_cfg_minb(int c) { return c == 0 ? 1 : 2; }
+
+template <int MODE, int CFG>
+inline cudaError_t lk_launch_cfg(const DLib& L, const int32_t* q, int64_t n, DSlots S, int32_t fused,
+                                 unsigned long long* cnt, const double* bE, const int32_t* bM, double* bout,
+                                 int sm_count, size_t smem, cudaStream_t st)
+{
+    constexpr int NW = lk_cfg_warps(CFG), MB = lk_cfg_minb(CFG);
+    constexpr int64_t chunk = (NW - 1) * 32;
+    const unsigned nb = (unsigned)std::min<int64_t>((n + chunk - 1) / chunk, (int64_t)sm_count * MB);
+    if (L.den_staged)
+        k_lookup_staged<MODE, true, NW, MB><<<nb, NW * 32, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM, bout);
+    else
+        k_lookup_staged<MODE, false, NW, MB><<<nb, NW * 32, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM, bout);
+    return cudaGetLastError();
+}
+
+template <int MODE>
+inline cudaError_t lk_launch(int cfg, const DLib& L, const int32_t* q, int64_t n, DSlots S, int32_t fused,
+                             unsigned long long* cnt, const double* bE, const int32_t* bM, double* bout, int sm_count,
+                             size_t smem, cudaStream_t st)
+{
+    switch (cfg) {
+    case 1: return lk_launch_cfg<MODE, 1>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st);
+    case 2: return lk_launch_cfg<MODE, 2>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st);
+    default: return lk_launch_cfg<MODE, 0>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st);
+    }
+}
+
+template <int MODE, int CFG>
+inline cudaError_t lk_set_smem_cfg(size_t smem)
+{
+    constexpr int NW = lk_cfg_warps(CFG), MB = lk_cfg_minb(CFG);
+    cudaError_t e = cudaFuncSetAttribute(k_lookup_staged<MODE, true, NW, MB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_lookup_staged<MODE, false, NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem);
+}
+
+inline cudaError_t lk_set_smem(size_t smem)
+{
+    cudaError_t e;
+    if ((e = lk_set_smem_cfg<0, 0>(smem)) || (e = lk_set_smem_cfg<0, 1>(smem)) || (e = lk_set_smem_cfg<0, 2>(smem)) ||
+        (e = lk_set_smem_cfg<1, 0>(smem)) || (e = lk_set_smem_cfg<1, 1>(smem)) || (e = lk_set_smem_cfg<1, 2>(smem)))
+        return e;
+    return cudaSuccess;
 }
 
 }  // namespace emc

@@ -39,7 +39,7 @@ def main():
     launches_csv, rep, tag = sys.argv[1], sys.argv[2], sys.argv[3]
     agg = launches(launches_csv)
     tot = sum(v[1] for v in agg.values())
-    lines = [f"# {tag}: ncu launch list (bench.py --steps 1 --warmup 1, C4, 40M particles)",
+    lines = [f"# {tag}: ncu launch list (bench.py --steps 1 --warmup 1 --no-cpu-baseline, C4, 40M particles)",
              "", "Per-launch device times are ncu-serialised and cold-cache: compare shares, not absolutes.",
              "", "| kernel | launches | total ms | share |", "|---|---:|---:|---:|"]
     for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
