@@ -19,8 +19,12 @@ e2e       = RunResult.active_rate of the same run_event() call: the
             reference's own metric definition (replication.py:282-304, host
             wall per batch incl. host merge/reduce/resample and the per-batch
             D2H of counters/tallies), i.e. through the public API.
-roofline  = XS-lookup kernel: algorithmic bytes = 64 B per (lookup, nuclide)
-            (grid pair + sigma_t/c/f pairs) / summed k_lookup time.
+roofline  = XS-lookup kernel (k_lookup_staged): algorithmic bytes = 64 B per
+            (lookup, nuclide) (grid pair + sigma_t/c/f pairs) / summed
+            lookup time.  The staged kernel re-reads each record from shared
+            memory for ~1000 particles, so achieved > HBM peak: the kernel is
+            bound by the shared-memory (L1TEX) data pipe and FP64 issue, not by
+            DRAM (see DESIGN.md section 4 and profiles/).
 """
 
 from __future__ import annotations
@@ -44,6 +48,7 @@ WORKLOAD = dict(workload="C4 HM-large depleted pincell: depleted_pincell(272,3,1
                 ppb_per_gpu=40_000_000, mode="event", reduction="fast", tally_mode="fused",
                 sort="on (mat, log E) every lookup sweep", seed=42)
 BYTES_PER_NUCLIDE_LOOKUP = 64
+TRAFFIC_PROFILE = "r1s2_lookup_traffic.json"
 
 
 def _peaks():
@@ -218,9 +223,12 @@ def run_ours(args):
     peak, peak_src = _peaks()
     lk_time = res.timings["lookup_active_s"] / ws if "lookup_active_s" in res.timings else None
     achieved = (BYTES_PER_NUCLIDE_LOOKUP * n_nl / ws) / lk_time / 1e9 if lk_time else None
+    # DRAM bytes per launch of the lookup kernel: ncu's dram__bytes_read+write
+    # summed over every lookup launch of one C4 batch, per nuclide-lookup
+    # (profiles/<round>_lookup_traffic.json), x this run's nuclide-lookups per launch
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_lookup_summary.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", TRAFFIC_PROFILE)) as fh:
             traffic = json.load(fh).get("dram_bytes_per_nuclide_lookup")
         if traffic is not None:
             traffic = traffic * (n_nl / ws) / max(1, res.timings.get("lookup_launches_active", 1) / ws)
@@ -240,7 +248,7 @@ def run_ours(args):
         "gpu_launches": int(launches0["end"] - launches0["n"]),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "k_lookup", "peak_source": peak_src,
+                     "kernel": "k_lookup_staged", "peak_source": peak_src,
                      "algorithmic_bytes": "64 B x nuclide-lookups (grid pair + sigma_t,c,f pairs)",
                      "nuclide_lookups_per_step": n_nl / args.steps},
         "clocks": sampler.summary(),

@@ -116,6 +116,10 @@ int emc_configure(emc_ctx *ctx, const emc_run_config *cfg);
  * x,y,z,dx,dy,dz,E of length n that stay valid during the next batch) */
 int emc_set_source_local(emc_ctx *ctx, double u);
 int emc_set_source_device(emc_ctx *ctx, const void *const ptrs[7], int64_t n, double u);
+/* same, when the arrays hold only the window of the global bank this rank
+ * resamples from: element j is global site (lo + j) mod n (multi-GPU bank
+ * exchange, replaces the R:221-228 gather + R:271-280 resample for a rank) */
+int emc_set_source_window(emc_ctx *ctx, const void *const ptrs[7], int64_t n, double u, int64_t lo);
 
 /* one worker-batch: replaces kernels.run_event_batch / run_history_batch
  * (kernels.py:1043-1211) as called at replication.py:127-138, including the

@@ -69,6 +69,7 @@ SYMBOLS = {
     "emc_configure": (C.c_int, [_P, C.POINTER(EmcRunConfig)]),
     "emc_set_source_local": (C.c_int, [_P, _D]),
     "emc_set_source_device": (C.c_int, [_P, C.POINTER(_P), _I64, _D]),
+    "emc_set_source_window": (C.c_int, [_P, C.POINTER(_P), _I64, _D, _I64]),
     "emc_run_batch": (C.c_int, [_P, C.POINTER(EmcBatchArgs), C.POINTER(EmcBatchResult)]),
     "emc_reduce_bins": (C.c_int, [_P, _P, _P, _I64]),
     "emc_bank_size": (C.c_int, [_P, C.POINTER(_I64)]),

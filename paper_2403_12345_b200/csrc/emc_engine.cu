@@ -490,7 +490,7 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
     c->cub_tmp.alloc(std::max<size_t>(t1, 1));
     (void)t2;
     c->bank_n = 0;
-    c->src = DSrc{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.0};
+    c->src = DSrc{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.0, 0};
     c->configured = true;
     return 0;
 }
@@ -500,7 +500,7 @@ extern "C" int emc_set_source_local(emc_ctx* c, double u)
     if (!c || !c->configured) return fail_arg("not configured");
     if (c->bank_n < 1) return fail_arg("no local bank to resample");
     SiteBufs& b = c->bank();
-    c->src = DSrc{b.x.p, b.y.p, b.z.p, b.dx.p, b.dy.p, b.dz.p, b.E.p, c->bank_n, u};
+    c->src = DSrc{b.x.p, b.y.p, b.z.p, b.dx.p, b.dy.p, b.dz.p, b.E.p, c->bank_n, u, 0};
     return 0;
 }
 
@@ -509,7 +509,16 @@ extern "C" int emc_set_source_device(emc_ctx* c, const void* const ptrs[7], int6
     if (!c || !c->configured || !ptrs) return fail_arg("emc_set_source_device: bad arguments");
     if (n < 1) return fail_arg("empty source bank");
     c->src = DSrc{(const double*)ptrs[0], (const double*)ptrs[1], (const double*)ptrs[2], (const double*)ptrs[3],
-                  (const double*)ptrs[4], (const double*)ptrs[5], (const double*)ptrs[6], n, u};
+                  (const double*)ptrs[4], (const double*)ptrs[5], (const double*)ptrs[6], n, u, 0};
+    return 0;
+}
+
+extern "C" int emc_set_source_window(emc_ctx* c, const void* const ptrs[7], int64_t n, double u, int64_t lo)
+{
+    int rc = emc_set_source_device(c, ptrs, n, u);
+    if (rc) return rc;
+    if (lo < 0 || lo >= n) return fail_arg("emc_set_source_window: lo outside the bank");
+    c->src.lo = lo;
     return 0;
 }
 

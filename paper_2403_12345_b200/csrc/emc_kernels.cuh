@@ -72,7 +72,8 @@ __device__ __forceinline__ bool source_particle(int32_t slot, int64_t g, const B
         double ue = draw(s, draws);
         a.E = clamp_energy(__dmul_rn(-bp.fission_t, emc_log(__dsub_rn(1.0, ue))), L, clamps);
     } else {
-        int64_t i = resample_index(g, src.n, bp.pmax, src.u);
+        int64_t i = resample_index(g, src.n, bp.pmax, src.u) - src.lo;
+        if (i < 0) i += src.n;                       // wrapped window (distributed.exchange_bank)
         a.x = src.x[i]; a.y = src.y[i]; a.z = src.z[i]; a.E = src.E[i];
         b.dx = src.dx[i]; b.dy = src.dy[i]; b.dz = src.dz[i];
     }

@@ -6,9 +6,12 @@ physics is assignment-invariant, acceptance criterion 2, and contiguous
 blocks make the canonical bank the rank-ordered concatenation of the
 rank-local canonical banks).  Per batch:
 
-  * fission bank: all-gather of per-rank site counts, then all-gather of the
-    canonical rank banks (NCCL over NVLink on GPU, gloo on CPU tests) into
-    one global bank every rank resamples from;
+  * fission bank: all-gather of per-rank site counts; every rank then needs
+    only the window of the global canonical bank its own particles resample
+    from (a contiguous, possibly wrapped range of ~1/W of the bank, computed
+    identically on every rank from the counts and the batch uniform), so the
+    sites move with one variable-size all-to-all (NCCL over NVLink on GPU,
+    gloo on CPU tests) instead of an all-gather of the whole bank;
   * tallies, deterministic: the canonical per-bin fold is chained through the
     ranks in order (rank r folds its log starting from rank r-1's partial
     sums), which is bit-identical to a single-rank fold -- then broadcast;
@@ -153,3 +156,96 @@ def device_view(ptr: int, n: int, dtype: str, device: int):
         }
 
     return torch.as_tensor(_Iface(), device=torch.device("cuda", device))
+
+
+def resample_index(g: int, n: int, ppb: int, u: float) -> int:
+    """Bank index particle g resamples (transport.py:188-200), with the same
+    IEEE double expression the device evaluates (floor(((g + u) * n) / ppb))."""
+    if n >= ppb:
+        i = int(np.floor(((float(g) + u) * float(n)) / float(ppb)))
+        return min(max(i, 0), n - 1)
+    return g % n
+
+
+def needed_window(g_lo: int, g_hi: int, n: int, ppb: int, u: float) -> tuple[int, int]:
+    """(lo, length): the particles [g_lo, g_hi) resample from bank indices
+    lo, lo+1, ..., lo+length-1 taken modulo n (resample_index is monotone in
+    g when n >= ppb, and g mod n otherwise)."""
+    if g_hi <= g_lo or n < 1:
+        return 0, 0
+    if n >= ppb:
+        a, b = resample_index(g_lo, n, ppb, u), resample_index(g_hi - 1, n, ppb, u)
+        return a, b - a + 1
+    if g_hi - g_lo >= n:
+        return 0, n
+    return g_lo % n, g_hi - g_lo
+
+
+def _segments(lo: int, length: int, n: int) -> list[tuple[int, int]]:
+    """Cyclic window -> up to two linear [a, b) ranges, in window order."""
+    if length <= 0:
+        return []
+    if lo + length <= n:
+        return [(lo, lo + length)]
+    return [(lo, n), (0, lo + length - n)]
+
+
+def exchange_bank(world: World, local_cols, counts: np.ndarray, ppb: int, u: float):
+    """Move to every rank the window of the global canonical bank its block
+    resamples from.  `local_cols`: this rank's canonical bank (any number of
+    same-length 1-D tensors, rank-ordered global offsets from `counts`).
+    Returns (window_cols, lo): window_cols[c][j] = global_col[c][(lo + j) % n]."""
+    import torch
+    import torch.distributed as dist
+    n = int(counts.sum())
+    offs = np.concatenate(([0], np.cumsum(counts))).astype(np.int64)
+    wins = [needed_window(*block_of(q, world.size, ppb), n, ppb, u) for q in range(world.size)]
+    if not world.distributed:
+        lo, length = wins[0]
+        segs = _segments(lo, length, n)
+        return [torch.cat([c[a:b] for a, b in segs]) if segs else c[:0] for c in local_cols], lo
+
+    def pieces(q: int, r: int) -> list[tuple[int, int]]:
+        """parts of rank r's bank that rank q needs, in q's window order (global indices)"""
+        out = []
+        for a, b in _segments(*wins[q], n):
+            lo_, hi_ = max(a, int(offs[r])), min(b, int(offs[r + 1]))
+            if hi_ > lo_:
+                out.append((lo_, hi_))
+        return out
+
+    me = world.rank
+    send_plan = [pieces(q, me) for q in range(world.size)]
+    recv_plan = [pieces(me, r) for r in range(world.size)]
+    send_splits = [sum(b - a for a, b in pl) for pl in send_plan]
+    recv_splits = [sum(b - a for a, b in pl) for pl in recv_plan]
+    # receive buffer order is rank-major; the window order is segment-major
+    seg_list = _segments(*wins[me], n)
+    order = []                      # (recv buffer offset, global a, global b)
+    pos = 0
+    for r in range(world.size):
+        for a, b in recv_plan[r]:
+            order.append((pos, a, b))
+            pos += b - a
+    dest = []                       # window offset of each received piece
+    for _, a, b in order:
+        wpos = 0
+        for sa, sb in seg_list:
+            if sa <= a < sb:
+                dest.append(wpos + (a - sa))
+                break
+            wpos += sb - sa
+    dev = _tensor_device(world)
+    out_cols = []
+    for col in local_cols:
+        col = col.to(dev)
+        base = int(offs[me])
+        send = torch.cat([col[a - base:b - base] for pl in send_plan for a, b in pl]) \
+            if sum(send_splits) else col[:0]
+        recv = torch.empty(sum(recv_splits), dtype=col.dtype, device=dev)
+        dist.all_to_all_single(recv, send.contiguous(), recv_splits, send_splits)
+        win = torch.empty_like(recv)
+        for (p, a, b), d in zip(order, dest):
+            win[d:d + (b - a)] = recv[p:p + (b - a)]
+        out_cols.append(win)
+    return out_cols, wins[me][0]

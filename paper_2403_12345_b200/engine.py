@@ -110,9 +110,14 @@ class DeviceEngine:
         N.check(self.lib.emc_set_source_local(self._h, u), "emc_set_source_local")
         self._src_keep = None
 
-    def set_source_device(self, ptrs, n: int, u: float, keep=None) -> None:
+    def set_source_device(self, ptrs, n: int, u: float, keep=None, lo: int | None = None) -> None:
+        """Resample the next batch from 7 device arrays (x..E): the whole
+        global bank (lo None) or the window starting at global site `lo`."""
         arr = (C.c_void_p * 7)(*[C.c_void_p(int(p)) for p in ptrs])
-        N.check(self.lib.emc_set_source_device(self._h, arr, n, u), "emc_set_source_device")
+        if lo is None:
+            N.check(self.lib.emc_set_source_device(self._h, arr, n, u), "emc_set_source_device")
+        else:
+            N.check(self.lib.emc_set_source_window(self._h, arr, n, u, int(lo)), "emc_set_source_window")
         self._src_keep = keep
 
     def run_batch(self, batch: int, k_run: float, batch0: bool, score: bool) -> BatchOutcome:

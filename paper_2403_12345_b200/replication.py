@@ -20,7 +20,8 @@ import numpy as np
 
 from . import prng, xslib
 from .distributed import (BANK_DTYPES, World, allgather_array, block_of, chained_fold,
-                          combine_counters, current_world, device_view, fast_bins, gather_bank)
+                          combine_counters, current_world, device_view, exchange_bank, fast_bins,
+                          gather_bank)
 from .engine import DeviceEngine
 from .errors import (ConfigurationError, EventMCError, GeometryError, PhysicsError,
                      PopulationCollapseError, RunawayHistoryError, StreamOverlapError)
@@ -100,7 +101,7 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
                "reduce": 0.0, "merge": 0.0}
     inactive_wall = active_wall = 0.0
     k_run = 1.0
-    last_bank_cols = None
+    last_local = last_counts = None
     launches = 0
     nuclide_lookups_active = 0
     act = dict(lookup_active_s=0.0, lookup_launches_active=0, h2d_bytes_active=0,
@@ -119,17 +120,17 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
                 cls, msg = _ERRORS[int(code)]
                 raise cls(f"{msg} (batch {b}, particle {int(gid)})")
 
-        # fission bank: global canonical order = rank-ordered concatenation
+        # fission bank: global canonical order = rank-ordered concatenation;
+        # each rank receives only the window its next batch resamples from
         t0 = time.perf_counter()
         counts = allgather_array(world, np.array([out.n_sites], np.int64))[:, 0]
         n_bank = int(counts.sum())
-        global_cols = None
+        local = None
         if world.distributed:
             local = [device_view(p, max(out.n_sites, 1), dt, eng.device)
                      for p, dt in zip(eng.bank_device_ptrs(), BANK_DTYPES)] \
                 if world.device_backend else \
                 [__import__("torch").as_tensor(c) for c in eng.bank_to_host()]
-            global_cols = gather_bank(world, local, counts)
         timings["merge"] += time.perf_counter() - t0
 
         # tallies + k
@@ -172,14 +173,17 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
                 raise PopulationCollapseError(f"no fission sites banked in batch {b}")
             u, _ = prng.next_uniform(prng.batch_stream(config.seed, b))
             if world.distributed:
-                src = global_cols[2:9]
-                eng.set_source_device([t.data_ptr() for t in src] if world.device_backend else
-                                      _host_to_device_bank(eng, src), n_bank, u, keep=src)
+                t0 = time.perf_counter()
+                src, lo = exchange_bank(world, local[2:9], counts, ppb, u)
+                if not world.device_backend:     # gloo (tests): stage the window on this GPU
+                    src = _host_to_device_bank(eng, src)
+                timings["merge"] += time.perf_counter() - t0
+                eng.set_source_device([t.data_ptr() for t in src], n_bank, u, keep=src, lo=lo)
             else:
                 eng.set_source_local(u)
             k_run = keff_values[b]
         else:
-            last_bank_cols = global_cols
+            last_local, last_counts = local, counts
         wall = time.perf_counter() - t_batch
         if on_batch is not None:
             on_batch(b, "end", eng)
@@ -188,9 +192,10 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
         else:
             inactive_wall += wall
 
-    # final canonical bank on the host
+    # final canonical bank on the host: the run's only full all-gather (every
+    # batch before moved just the resampling windows)
     if world.distributed:
-        cols = [c.cpu().numpy() for c in last_bank_cols]
+        cols = [c.cpu().numpy() for c in gather_bank(world, last_local, last_counts)]
     else:
         cols = list(eng.bank_to_host())
     bank = FissionBank(*cols)
@@ -218,8 +223,11 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
                      geometry_fingerprint=pincell.fingerprint())
 
 
-def _host_to_device_bank(eng, cols):   # pragma: no cover - gloo + GPU mix is not a product path
-    raise ConfigurationError("multi-rank transport needs the NCCL backend (one GPU per rank)")
+def _host_to_device_bank(eng, cols):
+    """gloo runs (the multi-rank GPU parity test: several ranks sharing one
+    GPU, where NCCL cannot run) exchange windows through host memory."""
+    import torch
+    return [c.to(torch.device("cuda", eng.device)).contiguous() for c in cols]
 
 
 @dataclass

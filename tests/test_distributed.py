@@ -93,3 +93,66 @@ def test_block_partition_covers_batch():
             blocks = [D.block_of(r, w, ppb) for r in range(w)]
             assert blocks[0][0] == 0 and blocks[-1][1] == ppb
             assert all(a[1] == b[0] for a, b in zip(blocks, blocks[1:]))
+
+
+def _xchg_worker(rank, world, port, q, counts, ppb, u):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = D.current_world()
+        counts = np.asarray(counts, np.int64)
+        n = int(counts.sum())
+        lo = int(counts[:rank].sum())
+        glob = torch.arange(n, dtype=torch.float64) * 1.5 + 0.25
+        mine = [glob[lo:lo + int(counts[rank])].clone(), -glob[lo:lo + int(counts[rank])].clone()]
+        win, wlo = D.exchange_bank(w, mine, counts, ppb, u)
+        g_lo, g_hi = D.block_of(rank, world, ppb)
+        ok = True
+        for g in range(g_lo, g_hi):
+            i = D.resample_index(g, n, ppb, u)
+            j = (i - wlo) % n
+            ok &= j < win[0].shape[0] and float(win[0][j]) == float(glob[i]) and float(win[1][j]) == -float(glob[i])
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("counts,ppb,u", [
+    ([30, 25, 41], 90, 0.37),      # bank larger than a batch: monotone windows
+    ([10, 0, 17], 60, 0.9),        # bank smaller than a batch: g mod n windows that wrap
+    ([5, 3, 2], 3, 0.01),          # tiny batch
+    ([0, 0, 7], 12, 0.5),          # all sites on one rank
+])
+def test_gloo_world3_bank_window_exchange(counts, ppb, u):
+    """Every rank receives exactly the bank window its particles resample
+    from (the device reads element (i - lo) mod n for global site i)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_xchg_worker, args=(r, 3, port, q, counts, ppb, u)) for r in range(3)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(3))
+    assert all(ok for _, ok in res), res
+
+
+def test_needed_window_covers_resample_indices():
+    rng = np.random.default_rng(1)
+    for _ in range(2000):
+        ppb = int(rng.integers(1, 200))
+        w = min(int(rng.integers(1, 9)), ppb)
+        n = int(rng.integers(1, 400))
+        u = float(rng.random())
+        for r in range(w):
+            lo, hi = D.block_of(r, w, ppb)
+            a, ln = D.needed_window(lo, hi, n, ppb, u)
+            need = {D.resample_index(g, n, ppb, u) for g in range(lo, hi)}
+            win = {(a + j) % n for j in range(ln)}
+            assert need <= win and len(win) == ln <= n
+            # tight: ~(block size) x n/ppb sites, i.e. ~1/W of the bank
+            bound = (hi - lo) * n // ppb + 2 if n >= ppb else min(n, hi - lo)
+            assert ln <= bound

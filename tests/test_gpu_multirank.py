@@ -1,0 +1,65 @@
+"""Multi-rank coordinator on the GPU: two ranks (gloo, sharing cuda:0 --
+NCCL cannot put two ranks on one GPU, and gpurun provides one) run the C1
+golden problem through run_replicated with the windowed bank exchange and
+the chained deterministic reduction.  Domain replication is
+partition-invariant (reference acceptance criterion 2), so both ranks must
+reproduce the reference's single-worker fingerprint bit for bit."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import golden_library
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank(rank, world, port, q, run, pm):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2403_12345_b200 as P
+        cell = P.Pincell(n_axial=pm["n_axial"], fuel_material_ids=pm["fuel_material_ids"],
+                         moderator_material_id=pm["moderator_material_id"])
+        cfg = P.RunConfig(**dict(run["config"], workers=world))
+        res = P.run_replicated(cfg, golden_library(run["problem"]), cell)
+        q.put((rank, res.physics_fingerprint(), res.keff.values.tolist(), len(res.bank)))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, f"error: {e!r}", None, None))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_multirank_matches_reference_fingerprint(golden, world):
+    run = golden["runs"]["c1_event"]
+    pm = golden["problems"]["c1"]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank, args=(r, world, port, q, run, pm)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(60)
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "run_c1_event.npz"))
+    for rank, fp, keff, nbank in res:
+        assert fp == run["fingerprint"], (rank, fp)
+        assert np.array_equal(np.array(keff), z["keff"])
+        assert nbank == run["bank_len"]
