@@ -107,6 +107,20 @@ int emc_set_stream(emc_ctx *ctx, void *cuda_stream);
 int emc_upload_library(emc_ctx *ctx, const emc_library *lib);
 /* replaces the geom tuple built at replication.py:171 */
 int emc_upload_geometry(emc_ctx *ctx, const emc_geometry *geom);
+/* Extensions beyond the reference (fixed-source shielding
+ * slab with 3D mesh flux tallies; parity pinned against the oracle's
+ * restatement of the same extension, not against the reference):
+ *   slab = 1: no fuel cylinder, the box is n_axial material layers in z;
+ *   vacuum = 1: outer box planes leak (counter 22) instead of reflecting;
+ *   fixed source: every batch samples a surface source on z = 0 (energy, or
+ *   the fission spectrum when energy == 0) instead of resampling a bank;
+ *   mesh: nx*ny*nz track-length (flux, total rate) tally over the box, one
+ *   batch's sums at emc_mesh_device() after each emc_run_batch (2 per cell). */
+int emc_set_geometry_options(emc_ctx *ctx, int32_t slab, int32_t vacuum);
+int emc_set_fixed_source(emc_ctx *ctx, int32_t enabled, double energy);
+int emc_set_mesh(emc_ctx *ctx, int32_t nx, int32_t ny, int32_t nz);
+int emc_mesh_device(emc_ctx *ctx, double **ptr, int64_t *n);
+
 /* replaces _Worker allocation (replication.py:62-111) */
 int emc_configure(emc_ctx *ctx, const emc_run_config *cfg);
 

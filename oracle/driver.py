@@ -60,7 +60,12 @@ class OLib(C.Structure):
 class OGeom(C.Structure):
     _fields_ = [("radius", C.c_double), ("r2", C.c_double), ("hp", C.c_double),
                 ("height", C.c_double), ("n_axial", C.c_int64),
-                ("zplanes", P), ("fuel_mats", P), ("mod_mat", C.c_int64)]
+                ("zplanes", P), ("fuel_mats", P), ("mod_mat", C.c_int64),
+                # extensions: slab, vacuum, mesh
+                ("slab", C.c_int32), ("vacuum", C.c_int32), ("mesh", P),
+                ("mnx", C.c_int32), ("mny", C.c_int32), ("mnz", C.c_int32), ("mpad", C.c_int32),
+                ("mx0", C.c_double), ("my0", C.c_double), ("mz0", C.c_double),
+                ("mdx", C.c_double), ("mdy", C.c_double), ("mdz", C.c_double)]
 
 
 class OSlots(C.Structure):
@@ -91,7 +96,8 @@ class OParams(C.Structure):
                 ("score", C.c_int32), ("use_logs", C.c_int32),
                 ("sort_enabled", C.c_int32), ("sort_every", C.c_int32),
                 ("batch0", C.c_int32), ("history", C.c_int32),
-                ("perturb_gid", C.c_int64)]
+                ("perturb_gid", C.c_int64),
+                ("fixed_source", C.c_int32), ("pad", C.c_int32), ("src_energy", C.c_double)]
 
 
 def build(force: bool = False) -> str:
@@ -155,14 +161,31 @@ class OracleLibrary:
 
 
 class OracleGeometry:
-    def __init__(self, geom):
+    """``geom`` = Pincell.as_tuple(); ``slab``/``vacuum`` and ``mesh``
+    (nx, ny, nz) are the extensions of SURVEY 8f row 1 (off by default).
+    With a mesh, ``self.mesh`` is this geometry's accumulator (one per worker:
+    see OracleGeometry.for_worker)."""
+
+    def __init__(self, geom, slab=False, vacuum=False, mesh=None):
         radius, r2, hp, height, n_axial, zplanes, fuel_mats, mod_mat = geom
+        self.args = (geom, slab, vacuum, mesh)
         self.keep = [np.ascontiguousarray(zplanes, np.float64),
                      np.ascontiguousarray(fuel_mats, np.int32)]
         self.n_axial = int(n_axial)
-        self.s = OGeom(float(radius), float(r2), float(hp), float(height),
+        hp, height = float(hp), float(height)
+        if mesh is not None:
+            nx, ny, nz = (int(v) for v in mesh)
+            self.mesh = np.zeros(2 * nx * ny * nz)
+            mptr, dims = _p(self.mesh), (nx, ny, nz, 0)
+            box = (-hp, -hp, 0.0, (2.0 * hp) / nx, (2.0 * hp) / ny, height / nz)
+        else:
+            self.mesh, mptr, dims, box = None, None, (0, 0, 0, 0), (0.0,) * 6
+        self.s = OGeom(float(radius), float(r2), hp, height,
                        int(n_axial), _p(self.keep[0]), _p(self.keep[1]),
-                       int(mod_mat))
+                       int(mod_mat), int(bool(slab)), int(bool(vacuum)), mptr, *dims, *box)
+
+    def for_worker(self):
+        return OracleGeometry(*self.args) if self.mesh is not None else self
 
 
 # ---- single-op wrappers (parity checks of the device ops) -------------------
@@ -259,6 +282,8 @@ def _run_worker(w: _Worker, olib, ogeom, src_s, params: OParams, n_bins):
         w.counters[:] = 0
         w.timings[:] = 0.0
         w.wbins[:] = 0.0
+        if ogeom.mesh is not None:
+            ogeom.mesh[:] = 0.0
         lib().oracle_run_batch(_p(w.assigned), C.c_int64(w.assigned.shape[0]),
                                C.byref(w.slots), C.byref(olib.s),
                                C.byref(ogeom.s), C.byref(src_s),
@@ -318,7 +343,10 @@ def run(cfg: dict, lib_arrays, geom, workers: int | None = None,
     active/inactive rates."""
     cfg = dict(DEFAULTS, **cfg)
     olib = OracleLibrary(lib_arrays)
-    ogeom = OracleGeometry(geom)
+    mesh = cfg.get("mesh")
+    ogeom = OracleGeometry(geom, slab=cfg.get("slab", False), vacuum=cfg.get("vacuum", False),
+                           mesh=mesh)
+    fixed = cfg.get("run_mode", "eigenvalue") == "fixed_source"
     ppb = int(cfg["particles_per_batch"])
     n_axial = ogeom.n_axial
     n_tally = (n_axial + 1) * 5
@@ -328,6 +356,10 @@ def run(cfg: dict, lib_arrays, geom, workers: int | None = None,
     nw = int(workers if workers is not None else cfg.get("workers", 1))
     ws = [_Worker(np.arange(w, ppb, nw, dtype=np.int64), cfg, olib.max_comp,
                   n_bins) for w in range(nw)]
+    wgeom = [ogeom.for_worker() for _ in ws]
+    mesh_sum = mesh_sq = None
+    if mesh is not None:
+        mesh_sum, mesh_sq = np.zeros_like(ogeom.mesh), np.zeros_like(ogeom.mesh)
     n_batches = int(cfg["inactive_batches"]) + int(cfg["active_batches"])
     n_inactive = int(cfg["inactive_batches"])
     batch_sums = np.zeros((n_batches, n_bins))
@@ -355,14 +387,21 @@ def run(cfg: dict, lib_arrays, geom, workers: int | None = None,
                              int(cfg.get("sort_enabled", True)),
                              int(cfg.get("sort_every_n", 1)), int(b == 0),
                              int(cfg["mode"] == "history"),
-                             int(cfg.get("perturb_particle", -1)))
+                             int(cfg.get("perturb_particle", -1)),
+                             int(fixed), 0, float(cfg.get("source_energy", 0.0)))
             if pool is not None:
-                futs = [pool.submit(_run_worker, w, olib, ogeom, src_s, params,
-                                    n_bins) for w in ws]
+                futs = [pool.submit(_run_worker, w, olib, g, src_s, params,
+                                    n_bins) for w, g in zip(ws, wgeom)]
                 for f in futs:
                     f.result()
             else:
-                _run_worker(ws[0], olib, ogeom, src_s, params, n_bins)
+                _run_worker(ws[0], olib, wgeom[0], src_s, params, n_bins)
+            if mesh is not None and active:
+                mb = np.zeros_like(mesh_sum)
+                for g in wgeom:
+                    mb += g.mesh
+                mesh_sum += mb
+                mesh_sq += mb * mb
             for w in ws:
                 err = int(w.counters[CNT["ERR"]])
                 if err:
@@ -396,10 +435,10 @@ def run(cfg: dict, lib_arrays, geom, workers: int | None = None,
             batch_sums[b] = sums
             keff[b] = sums[n_tally] / weight
             sourced = sum(int(w.counters[CNT["SOURCED"]]) for w in ws)
-            deaths = sum(int(w.counters[5]) + int(w.counters[6]) for w in ws)
+            deaths = sum(int(w.counters[5]) + int(w.counters[6]) + int(w.counters[22]) for w in ws)
             if sourced != ppb or deaths != ppb:
                 raise OracleError("EventMCError", "neutron bookkeeping broken")
-            for name, idx in COUNTER_SUMS:
+            for name, idx in COUNTER_SUMS + ((("leaks", 22),) if cfg.get("vacuum") else ()):
                 run_counters[name] = run_counters.get(name, 0) + sum(
                     int(w.counters[idx]) for w in ws)
             for name, idx in COUNTER_MAXES:
@@ -408,7 +447,9 @@ def run(cfg: dict, lib_arrays, geom, workers: int | None = None,
             for key, ti in (("lookup", 0), ("advance", 1), ("collision", 2),
                             ("sort", 3)):
                 timings[key] += sum(float(w.timings[ti]) for w in ws)
-            if b < n_batches - 1:
+            if b < n_batches - 1 and fixed:
+                pass                                # fixed source: sampled afresh every batch
+            elif b < n_batches - 1:
                 if bank[0].shape[0] == 0:
                     raise OracleError("PopulationCollapseError",
                                       f"no fission sites banked in batch {b}")
@@ -426,7 +467,14 @@ def run(cfg: dict, lib_arrays, geom, workers: int | None = None,
         if pool is not None:
             pool.shutdown(wait=False)
     n_active = n_batches - n_inactive
-    return dict(keff=keff, batch_sums=batch_sums, bank=bank,
+    mesh_out = {}
+    if mesh is not None:
+        nx, ny, nz = (int(v) for v in mesh)
+        mean = mesh_sum / weight / max(n_active, 1)
+        mesh_out = dict(mesh_mean=mean.reshape(nz, ny, nx, 2),
+                        mesh_sum=mesh_sum.reshape(nz, ny, nx, 2),
+                        mesh_sq=mesh_sq.reshape(nz, ny, nx, 2))
+    return dict(keff=keff, batch_sums=batch_sums, bank=bank, **mesh_out,
                 counters=run_counters, timings=timings,
                 inactive_wall=inactive_wall, active_wall=active_wall,
                 active_rate=(n_active * ppb / active_wall

@@ -31,11 +31,12 @@
 
 enum { SURF_CYL = 0, SURF_XMIN, SURF_XMAX, SURF_YMIN, SURF_YMAX, SURF_ZMIN, SURF_ZMAX, SURF_AXIAL_BASE };
 enum { KIND_FUEL = 0, KIND_MOD = 1 };
-enum { ROUTE_ERROR = -1, ROUTE_COLLISION = 0, ROUTE_LOOKUP = 1, OUT_SCATTER = 0, OUT_DIED = 1 };
+enum { ROUTE_ERROR = -1, ROUTE_COLLISION = 0, ROUTE_LOOKUP = 1, ROUTE_LEAK = 2, OUT_SCATTER = 0, OUT_DIED = 1 };
 enum { CNT_LOG_N = 0, CNT_SITE_N, CNT_OVF, CNT_ERR, CNT_ERR_AUX, CNT_CAPTURES, CNT_FISSIONS,
        CNT_SOURCED, CNT_MAX_DRAWS, CNT_CLAMPS, CNT_INTERP_TRANSPORT, CNT_INTERP_SCORE,
        CNT_EV_LOOKUP, CNT_EV_ADVANCE, CNT_EV_COLLISION, CNT_INV_LOOKUP, CNT_INV_ADVANCE,
-       CNT_INV_COLLISION, CNT_SORTS, CNT_MAX_INFLIGHT, CNT_MAX_HIST_LOG };
+       CNT_INV_COLLISION, CNT_SORTS, CNT_MAX_INFLIGHT, CNT_MAX_HIST_LOG, CNT_NUCLIDE_LOOKUPS,
+       CNT_LEAKS };
 enum { ERR_NO_SURFACE = 1, ERR_OUTSIDE_BOX, ERR_STREAM_OVERLAP, ERR_RUNAWAY_HISTORY,
        ERR_QUEUE_STATE, ERR_NONPOSITIVE_SIGMA };
 enum { TM_LOOKUP = 0, TM_ADVANCE, TM_COLLISION, TM_SORT };
@@ -51,6 +52,11 @@ typedef struct {
 typedef struct {
     double radius, r2, hp, height; int64_t n_axial;
     const double *zplanes; const int32_t *fuel_mats; int64_t mod_mat;
+    /* extensions (not in the reference): slab layers, vacuum
+     * boundaries, track-length mesh (mesh == NULL: off) */
+    int32_t slab, vacuum;
+    double *mesh; int32_t mnx, mny, mnz, mpad;
+    double mx0, my0, mz0, mdx, mdy, mdz;
 } OGeom;
 
 typedef struct {
@@ -77,6 +83,7 @@ typedef struct {
     uint64_t seed; int64_t batch, pmax; double alpha, fission_t, k_run;
     int32_t fused, score, use_logs, sort_enabled, sort_every, batch0, history;
     int64_t perturb_gid;
+    int32_t fixed_source, pad; double src_energy;     /* extension: fixed surface source */
 } OParams;
 
 static double now_s(void) {
@@ -114,7 +121,7 @@ void oracle_locate(double x, double y, double z, const OGeom *g, int64_t *out3) 
     if (x < -g->hp || x > g->hp || y < -g->hp || y > g->hp || z < 0.0 || z > g->height) {
         out3[0] = out3[1] = out3[2] = -1; return;
     }
-    if (x * x + y * y < g->r2) {
+    if (g->slab || x * x + y * y < g->r2) {
         int64_t a = axial_index(z, g->n_axial, g->height);
         out3[0] = KIND_FUEL; out3[1] = a; out3[2] = g->fuel_mats[a]; return;
     }
@@ -126,7 +133,12 @@ double oracle_boundary_distance(double x, double y, double z, double ux, double 
     double best = INFINITY, t; int64_t surf = -1;
     double a = ux * ux + uy * uy;
     if (kd == KIND_FUEL) {
-        if (a > 0.0) {
+        if (g->slab) {    /* extension: slab layer bounded by the box side planes */
+            if (ux > 0.0) { t = (g->hp - x) / ux; if (t > DIST_EPS && t < best) { best = t; surf = SURF_XMAX; } }
+            else if (ux < 0.0) { t = (-g->hp - x) / ux; if (t > DIST_EPS && t < best) { best = t; surf = SURF_XMIN; } }
+            if (uy > 0.0) { t = (g->hp - y) / uy; if (t > DIST_EPS && t < best) { best = t; surf = SURF_YMAX; } }
+            else if (uy < 0.0) { t = (-g->hp - y) / uy; if (t > DIST_EPS && t < best) { best = t; surf = SURF_YMIN; } }
+        } else if (a > 0.0) {
             double b = 2.0 * (x * ux + y * uy), c = x * x + y * y - g->r2;
             double disc = b * b - 4.0 * a * c;
             if (disc > 0.0) { t = (-b + sqrt(disc)) / (2.0 * a); if (t > DIST_EPS && t < best) { best = t; surf = SURF_CYL; } }
@@ -272,6 +284,42 @@ static void reassemble_tcf(double E, int64_t m, const OLib *L, double *o4) {
     o4[0] = st; o4[1] = sc; o4[2] = sf; o4[3] = snf;
 }
 
+/* Extension: track-length mesh estimator, the same 3D DDA
+ * and operation order as the device (csrc/emc_device.cuh: score_mesh). */
+static inline int32_t mesh_cell(double v, double v0, double dv, int32_t n) {
+    int32_t i = (int32_t)floor((v - v0) / dv);
+    return i < 0 ? 0 : (i > n - 1 ? n - 1 : i);
+}
+static inline double mesh_next(double v, double u, int32_t i, double v0, double dv) {
+    if (u > 0.0) return ((v0 + (double)(i + 1) * dv) - v) / u;
+    if (u < 0.0) return ((v0 + (double)i * dv) - v) / u;
+    return INFINITY;
+}
+static void mesh_score(const OGeom *G, double x, double y, double z, double ux, double uy, double uz,
+                       double ell, double sig_t) {
+    int32_t ix = mesh_cell(x, G->mx0, G->mdx, G->mnx), iy = mesh_cell(y, G->my0, G->mdy, G->mny),
+            iz = mesh_cell(z, G->mz0, G->mdz, G->mnz);
+    double t = 0.0;
+    for (;;) {
+        double tx = mesh_next(x, ux, ix, G->mx0, G->mdx), ty = mesh_next(y, uy, iy, G->my0, G->mdy),
+               tz = mesh_next(z, uz, iz, G->mz0, G->mdz);
+        double tn = tx < ty ? tx : ty;
+        tn = tz < tn ? tz : tn;
+        int last = !(tn < ell);
+        if (last) tn = ell;
+        double seg = tn - t;
+        if (seg > 0.0) {
+            double *a = G->mesh + 2 * (((int64_t)iz * G->mny + iy) * G->mnx + ix);
+            a[0] += seg; a[1] += seg * sig_t;
+        }
+        if (last) break;
+        if (tx == tn) { ix += ux > 0.0 ? 1 : -1; if (ix < 0 || ix >= G->mnx) break; }
+        else if (ty == tn) { iy += uy > 0.0 ? 1 : -1; if (iy < 0 || iy >= G->mny) break; }
+        else { iz += uz > 0.0 ? 1 : -1; if (iz < 0 || iz >= G->mnz) break; }
+        if (tn > t) t = tn;
+    }
+}
+
 /* K:713-811 */
 static int op_advance(int64_t i, const OSlots *S, const OLib *L, const OGeom *G, OLog *lg, double *wbins,
                       int64_t *cnt, int score, int fused, int use_logs) {
@@ -309,9 +357,11 @@ static int op_advance(int64_t i, const OSlots *S, const OLib *L, const OGeom *G,
             wbins[base + 0] += fl; wbins[base + 1] += v_tot; wbins[base + 2] += v_abs;
             wbins[base + 3] += v_fis; wbins[base + 4] += v_nsf;
         }
+        if (G->mesh) mesh_score(G, S->px[i], S->py[i], S->pz[i], S->dx[i], S->dy[i], S->dz[i], ell, sig_t);
     }
     S->px[i] += S->dx[i] * ell; S->py[i] += S->dy[i] * ell; S->pz[i] += S->dz[i] * ell;
     if (!crossing) return ROUTE_COLLISION;
+    if (G->vacuum && surf >= SURF_XMIN && surf <= SURF_ZMAX) { cnt[CNT_LEAKS] += 1; return ROUTE_LEAK; }
     if (surf >= SURF_XMIN && surf <= SURF_ZMAX) {
         if (surf == SURF_XMIN || surf == SURF_XMAX) S->dx[i] = -S->dx[i];
         else if (surf == SURF_YMIN || surf == SURF_YMAX) S->dy[i] = -S->dy[i];
@@ -414,7 +464,14 @@ static int op_source(int64_t i, int64_t g, const OSlots *S, const OLib *L, const
     uint64_t s0 = oracle_lcg_skip(P->seed, offset);
     if (g == P->perturb_gid) s0 ^= 1ULL;
     S->rng[i] = s0; S->draws[i] = 0; S->ordctr[i] = 0; S->histlog[i] = 0; S->gid[i] = g; S->wt[i] = 1.0;
-    if (P->batch0) {
+    if (P->fixed_source) {    /* extension: surface source on z = 0, mu = u inward */
+        double u1 = draw(S, i), u2 = draw(S, i);
+        S->px[i] = (2.0 * u1 - 1.0) * G->hp; S->py[i] = (2.0 * u2 - 1.0) * G->hp; S->pz[i] = 0.0;
+        double mu = draw(S, i), phi = TWO_PI * draw(S, i), sn = sqrt(1.0 - mu * mu);
+        S->dx[i] = sn * cos(phi); S->dy[i] = sn * sin(phi); S->dz[i] = mu;
+        if (P->src_energy > 0.0) S->en[i] = P->src_energy;
+        else { double ue = draw(S, i); S->en[i] = clamp_energy(-P->fission_t * log(1.0 - ue), L, cnt); }
+    } else if (P->batch0) {
         double x, y;
         for (;;) {
             double u1 = draw(S, i), u2 = draw(S, i);
@@ -478,6 +535,7 @@ static void run_history_batch(const int64_t *assigned, int64_t n_assigned, const
             double t2 = now_s(); tm[TM_ADVANCE] += t2 - t1;
             cnt[CNT_EV_ADVANCE] += 1; cnt[CNT_INV_ADVANCE] += 1;
             if (r == ROUTE_ERROR) return;
+            if (r == ROUTE_LEAK) alive = 0;
             if (r == ROUTE_COLLISION) {
                 int rc = op_collision(0, S, L, lg, sb, wbins, cnt, P, nbins - 1);
                 double t3 = now_s(); tm[TM_COLLISION] += t3 - t2;
@@ -526,7 +584,14 @@ static void run_event_batch(const int64_t *assigned, int64_t n_assigned, const O
                 int r = op_advance(s, S, L, G, lg, wbins, cnt, P->score, P->fused, P->use_logs);
                 if (r == ROUTE_ERROR) goto done;
                 if (S->draws[s] >= (int64_t)STRIDE) { cnt[CNT_ERR] = ERR_STREAM_OVERLAP; cnt[CNT_ERR_AUX] = S->gid[s]; goto done; }
-                if (r == ROUTE_COLLISION) q_col[nc++] = s; else q_look[nl++] = s;
+                if (r == ROUTE_COLLISION) q_col[nc++] = s;
+                else if (r == ROUTE_LEAK) {             /* extension: vacuum leakage ends the history */
+                    finish_history(s, S, cnt); inflight--;
+                    if (cursor < n_assigned) {
+                        if (op_source(s, assigned[cursor], S, L, G, src, P, cnt) < 0) goto done;
+                        cursor++; inflight++; cnt[CNT_SOURCED] += 1; q_look[nl++] = s;
+                    }
+                } else q_look[nl++] = s;
             }
             tm[TM_ADVANCE] += now_s() - t0;
             cnt[CNT_EV_ADVANCE] += n_sweep; cnt[CNT_INV_ADVANCE] += 1; na = 0;

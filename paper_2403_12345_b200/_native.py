@@ -67,6 +67,10 @@ SYMBOLS = {
     "emc_upload_library": (C.c_int, [_P, C.POINTER(EmcLibrary)]),
     "emc_upload_geometry": (C.c_int, [_P, C.POINTER(EmcGeometry)]),
     "emc_configure": (C.c_int, [_P, C.POINTER(EmcRunConfig)]),
+    "emc_set_geometry_options": (C.c_int, [_P, _I32, _I32]),
+    "emc_set_fixed_source": (C.c_int, [_P, _I32, _D]),
+    "emc_set_mesh": (C.c_int, [_P, _I32, _I32, _I32]),
+    "emc_mesh_device": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_I64)]),
     "emc_set_source_local": (C.c_int, [_P, _D]),
     "emc_set_source_device": (C.c_int, [_P, C.POINTER(_P), _I64, _D]),
     "emc_set_source_window": (C.c_int, [_P, C.POINTER(_P), _I64, _D, _I64]),

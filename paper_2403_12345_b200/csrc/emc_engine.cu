@@ -122,6 +122,12 @@ struct emc_ctx {
     DBuf<double> zplanes; DBuf<int32_t> fuel_mats;
     DGeom G{};
 
+    // extensions: fixed surface source, track-length mesh
+    int32_t fixed_source = 0;
+    double src_energy = 0.0;
+    DBuf<double> mesh_acc;
+    DMesh M{};
+
     // run configuration
     bool configured = false;
     emc_run_config cfg{};
@@ -387,10 +393,50 @@ extern "C" int emc_upload_geometry(emc_ctx* c, const emc_geometry* g)
     EMC_TRY_CUDA(cudaMemcpy(c->zplanes.p, g->zplanes, (g->n_axial + 1) * 8, cudaMemcpyHostToDevice));
     EMC_TRY_CUDA(cudaMemcpy(c->fuel_mats.p, g->fuel_mats, g->n_axial * 4, cudaMemcpyHostToDevice));
     c->G = DGeom{g->radius, g->r2, g->half_pitch, g->height, (int32_t)g->n_axial, (int32_t)g->mod_mat,
-                 c->zplanes.p, c->fuel_mats.p};
+                 c->zplanes.p, c->fuel_mats.p, 0, 0};
+    c->M.on = 0;
     c->n_bins = (int32_t)((g->n_axial + 1) * 5 + 1);
     c->kbin = c->n_bins - 1;
     c->have_geom = true;
+    return 0;
+}
+
+extern "C" int emc_set_geometry_options(emc_ctx* c, int32_t slab, int32_t vacuum)
+{
+    if (!c || !c->have_geom) return fail_arg("emc_set_geometry_options: upload the geometry first");
+    c->G.slab = slab ? 1 : 0;
+    c->G.vacuum = vacuum ? 1 : 0;
+    return 0;
+}
+
+extern "C" int emc_set_fixed_source(emc_ctx* c, int32_t enabled, double energy)
+{
+    if (!c) return fail_arg("null ctx");
+    if (enabled && !(energy >= 0.0)) return fail_arg("fixed source energy must be >= 0 (0: fission spectrum)");
+    c->fixed_source = enabled ? 1 : 0;
+    c->src_energy = energy;
+    return 0;
+}
+
+extern "C" int emc_set_mesh(emc_ctx* c, int32_t nx, int32_t ny, int32_t nz)
+{
+    if (!c || !c->have_geom) return fail_arg("emc_set_mesh: upload the geometry first");
+    if (nx <= 0 || ny <= 0 || nz <= 0) { c->M.on = 0; return 0; }
+    const int64_t cells = (int64_t)nx * ny * nz;
+    if (cells > (int64_t)1 << 28) return fail_arg("mesh too large");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    if (c->mesh_acc.alloc(2 * cells)) return EMC_E_OOM;
+    EMC_TRY_CUDA(cudaMemset(c->mesh_acc.p, 0, 2 * cells * sizeof(double)));
+    const double hp = c->G.hp, h = c->G.height;
+    c->M = DMesh{c->mesh_acc.p, nx, ny, nz, 1, -hp, -hp, 0.0, (2.0 * hp) / nx, (2.0 * hp) / ny, h / nz};
+    return 0;
+}
+
+extern "C" int emc_mesh_device(emc_ctx* c, double** ptr, int64_t* n)
+{
+    if (!c || !ptr || !n) return fail_arg("emc_mesh_device: null argument");
+    *ptr = c->M.on ? c->M.acc : nullptr;
+    *n = c->M.on ? 2 * (int64_t)c->M.nx * c->M.ny * c->M.nz : 0;
     return 0;
 }
 
@@ -565,13 +611,17 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
     bp.perturb_gid = cf.perturb_gid; bp.alpha = cf.alpha; bp.fission_t = cf.fission_t; bp.k_run = a->k_run;
     bp.fused = cf.fused; bp.score = a->score; bp.use_logs = cf.use_logs; bp.batch0 = a->batch0;
     bp.kbin = c->kbin; bp.history = cf.history;
-    if (!a->batch0 && (c->src.n < 1 || !c->src.x)) return fail_arg("batch > 0 needs a source bank (emc_set_source_*)");
+    bp.fixed_source = c->fixed_source; bp.src_energy = c->src_energy;
+    if (!a->batch0 && !c->fixed_source && (c->src.n < 1 || !c->src.x))
+        return fail_arg("batch > 0 needs a source bank (emc_set_source_*)");
 
     DSites sv = c->sites.view();
     DLog lg{c->lg_gid.p, c->lg_ord.p, c->lg_bin.p, c->lg_val.p, (int64_t)c->lg_gid.n};
 
     EMC_TRY_CUDA(cudaMemsetAsync(c->cnt.p, 0, EMC_N_COUNTERS * sizeof(unsigned long long), st));
     EMC_TRY_CUDA(cudaMemsetAsync(c->bins.p, 0, c->n_bins * sizeof(double), st));
+    if (c->M.on)
+        EMC_TRY_CUDA(cudaMemsetAsync(c->M.acc, 0, 2 * (size_t)c->M.nx * c->M.ny * c->M.nz * sizeof(double), st));
     Ctl z{};
     const int64_t n0 = std::min<int64_t>(c->nslots, cf.n_assigned);
     z.cursor = (unsigned long long)n0;
@@ -590,7 +640,7 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
         EMC_TRY_CUDA(cudaEventRecord(c->ev[0], st));
         int64_t nthr = n0;
         k_history<<<(unsigned)((nthr + 127) / 128), 128, 0, st>>>(bp, c->L, c->G, c->src, c->S, lg, sv, c->bins.p,
-                                                                   c->ctl.p, c->cnt.p, nthr);
+                                                                   c->ctl.p, c->cnt.p, nthr, c->M);
         EMC_CHECK_LAUNCH(c);
         EMC_TRY_CUDA(cudaEventRecord(c->ev[1], st));
         EMC_TRY_CUDA(cudaMemcpyAsync(c->ctl_host, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
@@ -660,9 +710,10 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             EMC_CHECK_LAUNCH(c);
             EMC_TRY_CUDA(cudaEventRecord(c->ev[2], st));
             k_advance<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(q, (int32_t)nL, bp, c->L, c->G, c->S, lg, c->bins.p,
-                                                              c->qc.p, c->qx.p, c->ctl.p, c->cnt.p);
+                                                              c->qc.p, c->qx.p, c->ctl.p, c->cnt.p, c->M);
             EMC_CHECK_LAUNCH(c);
-            k_crossing<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(c->qx.p, &c->ctl.p->nX, c->G, c->S, nxt, c->ctl.p);
+            k_crossing<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(c->qx.p, &c->ctl.p->nX, bp, c->L, c->G, c->src, c->S,
+                                                               nxt, c->ctl.p, c->cnt.p);
             EMC_CHECK_LAUNCH(c);
             EMC_TRY_CUDA(cudaEventRecord(c->ev[3], st));
             k_collision<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(c->qc.p, &c->ctl.p->nC, bp, c->L, c->G, c->src,

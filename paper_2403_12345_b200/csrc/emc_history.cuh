@@ -11,12 +11,12 @@ namespace emc {
 
 __global__ void __launch_bounds__(128) k_history(BatchP bp, DLib L, DGeom G, DSrc src, DSlots S, DLog lg,
                                                  DSites sb, double* bins, Ctl* ctl, unsigned long long* cnt,
-                                                 int64_t nthreads)
+                                                 int64_t nthreads, DMesh M)
 {
     const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (slot >= nthreads) return;
     unsigned long long ev_l = 0, ev_a = 0, ev_c = 0, interp = 0, interp_score = 0, nuc_lookups = 0;
-    unsigned long long captures = 0, fissions = 0, sourced = 0, maxdraws = 0, maxhist = 0;
+    unsigned long long captures = 0, fissions = 0, sourced = 0, maxdraws = 0, maxhist = 0, leaks = 0;
     int clamps = 0;
     const int32_t s = (int32_t)slot;
     for (;;) {
@@ -78,12 +78,15 @@ __global__ void __launch_bounds__(128) k_history(BatchP bp, DLib L, DGeom G, DSr
                     }
                 }
                 if (hist > kMaxHistLog) { set_error(ctl, cnt, ERR_RUNAWAY_HISTORY, g); fail = true; break; }
+                if (M.on) score_mesh(M, x, y, z, dx, dy, dz, ell, st);
             }
             x = __dadd_rn(x, __dmul_rn(dx, ell));
             y = __dadd_rn(y, __dmul_rn(dy, ell));
             z = __dadd_rn(z, __dmul_rn(dz, ell));
             bool died = false;
-            if (crossing) {
+            if (crossing && G.vacuum && surf >= SURF_XMIN && surf <= SURF_ZMAX) {
+                leaks += 1; died = true;                 // vacuum boundary (extension)
+            } else if (crossing) {
                 if (surf >= SURF_XMIN && surf <= SURF_ZMAX) {
                     if (surf == SURF_XMIN || surf == SURF_XMAX) dx = -dx;
                     else if (surf == SURF_YMIN || surf == SURF_YMAX) dy = -dy;
@@ -171,6 +174,7 @@ __global__ void __launch_bounds__(128) k_history(BatchP bp, DLib L, DGeom G, DSr
     if (interp_score) atomicAdd(cnt + CNT_INTERP_SCORE, interp_score);
     if (captures) atomicAdd(cnt + CNT_CAPTURES, captures);
     if (fissions) atomicAdd(cnt + CNT_FISSIONS, fissions);
+    if (leaks) atomicAdd(cnt + CNT_LEAKS, leaks);
     if (sourced) atomicAdd(cnt + CNT_SOURCED, sourced);
     if (clamps) atomicAdd(cnt + CNT_CLAMPS, (unsigned long long)clamps);
     if (maxdraws) atomicMax(cnt + CNT_MAX_DRAWS, maxdraws);

@@ -56,7 +56,25 @@ __device__ __forceinline__ bool source_particle(int32_t slot, int64_t g, const B
     if (g == bp.perturb_gid) s ^= 1ULL;
     int32_t draws = 0;
     P0 a; P1 b;
-    if (bp.batch0) {
+    if (bp.fixed_source) {
+        // fixed surface source (extension): uniform on the
+        // z = 0 face, inward direction with mu = u (uniform in [0,1)), energy
+        // fixed or from the fission spectrum
+        double u1 = draw(s, draws), u2 = draw(s, draws);
+        a.x = __dmul_rn(__dsub_rn(__dmul_rn(2.0, u1), 1.0), G.hp);
+        a.y = __dmul_rn(__dsub_rn(__dmul_rn(2.0, u2), 1.0), G.hp);
+        a.z = 0.0;
+        const double mu = draw(s, draws), phi = __dmul_rn(kTwoPi, draw(s, draws));
+        const double sn = __dsqrt_rn(__dsub_rn(1.0, __dmul_rn(mu, mu)));
+        b.dx = __dmul_rn(sn, emc_cos(phi));
+        b.dy = __dmul_rn(sn, emc_sin(phi));
+        b.dz = mu;
+        if (bp.src_energy > 0.0) a.E = bp.src_energy;
+        else {
+            double ue = draw(s, draws);
+            a.E = clamp_energy(__dmul_rn(-bp.fission_t, emc_log(__dsub_rn(1.0, ue))), L, clamps);
+        }
+    } else if (bp.batch0) {
         double x, y;
         for (;;) {
             double u1 = draw(s, draws), u2 = draw(s, draws);
@@ -293,7 +311,7 @@ __device__ __forceinline__ void score_bins(double* bins, bool valid, int32_t bas
 __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __restrict__ q, int32_t n, BatchP bp,
                                                  DLib L, DGeom G, DSlots S, DLog lg, double* bins,
                                                  int32_t* q_col, int32_t* q_cross, Ctl* ctl,
-                                                 unsigned long long* cnt)
+                                                 unsigned long long* cnt, DMesh M)
 {
     unsigned long long interp_score = 0;
     EMC_WARP_LOOP(n) {
@@ -344,6 +362,7 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
                         v[0] = fl;
                         #pragma unroll
                         for (int k = 0; k < 5; ++k) nlog += v[k] != 0.0;
+                        if (M.on) score_mesh(M, a.x, a.y, a.z, b.dx, b.dy, b.dz, ell, sig_t);
                     }
                     a.x = __dadd_rn(a.x, __dmul_rn(b.dx, ell));
                     a.y = __dadd_rn(a.y, __dmul_rn(b.dy, ell));
@@ -397,38 +416,65 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
 // ---------------------------------------------------- surface crossing ---
 
 // K:782-811 (second half of the reference advance): reflect on the outer
-// box planes, nudge past the surface, update cell and material.
+// box planes, nudge past the surface, update cell and material.  With vacuum
+// boundaries (extension) an outer-plane crossing ends the history (leakage)
+// and the slot is refilled from the batch cursor like a collision death.
 __global__ void __launch_bounds__(256, EMC_COL_MINB) k_crossing(const int32_t* __restrict__ q, const unsigned int* nq,
-                                                  DGeom G, DSlots S, int32_t* q_next, Ctl* ctl)
+                                                  BatchP bp, DLib L, DGeom G, DSrc src, DSlots S, int32_t* q_next,
+                                                  Ctl* ctl, unsigned long long* cnt)
 {
     const int32_t n = (int32_t)*nq;
+    unsigned long long leaks = 0, sourced = 0, maxdraws = 0, maxhist = 0;
+    int clamps = 0;
     EMC_WARP_LOOP(n) {
         int64_t i = emc_base_ + lane_id();
-        bool valid = i < n;
+        bool valid = i < n, died = false;
         int32_t s = valid ? q[i] : 0;
         if (valid) {
             PState& p = S.ps[s];
             P0 a = p.a; P1 b = p.b; P3 d = p.d;
             const int32_t surf = d.surf;
-            if (surf >= SURF_XMIN && surf <= SURF_ZMAX) {
-                if (surf == SURF_XMIN || surf == SURF_XMAX) b.dx = -b.dx;
-                else if (surf == SURF_YMIN || surf == SURF_YMAX) b.dy = -b.dy;
-                else b.dz = -b.dz;
+            if (surf >= SURF_XMIN && surf <= SURF_ZMAX && G.vacuum) {
+                died = true;
+                leaks += 1;
+                maxdraws = max(maxdraws, (unsigned long long)d.draws);
+                maxhist = max(maxhist, (unsigned long long)d.histlog);
+            } else {
+                if (surf >= SURF_XMIN && surf <= SURF_ZMAX) {
+                    if (surf == SURF_XMIN || surf == SURF_XMAX) b.dx = -b.dx;
+                    else if (surf == SURF_YMIN || surf == SURF_YMAX) b.dy = -b.dy;
+                    else b.dz = -b.dz;
+                }
+                a.x = __dadd_rn(a.x, __dmul_rn(b.dx, kNudge));
+                a.y = __dadd_rn(a.y, __dmul_rn(b.dy, kNudge));
+                a.z = __dadd_rn(a.z, __dmul_rn(b.dz, kNudge));
+                if (surf == SURF_CYL) {
+                    if (d.kind == KIND_FUEL) { d.kind = KIND_MOD; d.axial = -1; }
+                    else { d.kind = KIND_FUEL; d.axial = axial_index(a.z, G.n_axial, G.height); }
+                } else if (surf >= SURF_AXIAL_BASE) {
+                    int32_t jpl = surf - SURF_AXIAL_BASE;
+                    d.axial = b.dz > 0.0 ? jpl : jpl - 1;
+                }
+                d.mat = d.kind == KIND_FUEL ? G.fuel_mats[d.axial] : G.mod_mat;
+                p.a = a; p.b = b; p.d = d;
             }
-            a.x = __dadd_rn(a.x, __dmul_rn(b.dx, kNudge));
-            a.y = __dadd_rn(a.y, __dmul_rn(b.dy, kNudge));
-            a.z = __dadd_rn(a.z, __dmul_rn(b.dz, kNudge));
-            if (surf == SURF_CYL) {
-                if (d.kind == KIND_FUEL) { d.kind = KIND_MOD; d.axial = -1; }
-                else { d.kind = KIND_FUEL; d.axial = axial_index(a.z, G.n_axial, G.height); }
-            } else if (surf >= SURF_AXIAL_BASE) {
-                int32_t jpl = surf - SURF_AXIAL_BASE;
-                d.axial = b.dz > 0.0 ? jpl : jpl - 1;
-            }
-            d.mat = d.kind == KIND_FUEL ? G.fuel_mats[d.axial] : G.mod_mat;
-            p.a = a; p.b = b; p.d = d;
         }
-        queue_push(q_next, &ctl->nL2, s, valid);
+        bool refill = false;
+        if (G.vacuum) {          // warp-uniform: the claim below needs all lanes
+            unsigned long long idx = warp_claim(&ctl->cursor, died ? 1u : 0u);
+            if (died && idx < (unsigned long long)bp.n_assigned) {
+                refill = source_particle(s, bp.g_lo + (int64_t)idx, bp, L, G, src, S, ctl, clamps);
+                sourced += 1;
+            }
+        }
+        queue_push(q_next, &ctl->nL2, s, (valid && !died) || refill);
+    }
+    if (G.vacuum) {
+        warp_add_u64(cnt + CNT_LEAKS, leaks);
+        warp_add_u64(cnt + CNT_SOURCED, sourced);
+        warp_add_u64(cnt + CNT_CLAMPS, (unsigned long long)clamps);
+        warp_max_u64(cnt + CNT_MAX_DRAWS, maxdraws);
+        warp_max_u64(cnt + CNT_MAX_HIST_LOG, maxhist);
     }
 }
 

@@ -105,6 +105,23 @@ class DeviceEngine:
                              config.fission_temperature, int(config.perturb_particle))
         N.check(self.lib.emc_configure(self._h, C.byref(cfg)), "emc_configure")
 
+    def set_extensions(self, pincell, config) -> None:
+        """Slab/vacuum geometry, fixed source and mesh tally (extensions,
+        SURVEY 8f row 1); applied on every run because engines are reused."""
+        N.check(self.lib.emc_set_geometry_options(self._h, int(pincell.is_slab),
+                                                  int(pincell.boundary == "vacuum")),
+                "emc_set_geometry_options")
+        N.check(self.lib.emc_set_fixed_source(self._h, int(config.run_mode == "fixed_source"),
+                                              float(config.source_energy)), "emc_set_fixed_source")
+        nx, ny, nz = (int(v) for v in config.mesh) if config.mesh is not None else (0, 0, 0)
+        N.check(self.lib.emc_set_mesh(self._h, nx, ny, nz), "emc_set_mesh")
+
+    def mesh_device(self) -> tuple[int, int]:
+        """(device pointer, length) of this batch's mesh sums (2 per cell)."""
+        p, n = C.c_void_p(), C.c_int64()
+        N.check(self.lib.emc_mesh_device(self._h, C.byref(p), C.byref(n)), "emc_mesh_device")
+        return int(p.value or 0), int(n.value)
+
     # ------------------------------------------------------------ batches
     def set_source_local(self, u: float) -> None:
         N.check(self.lib.emc_set_source_local(self._h, u), "emc_set_source_local")

@@ -7,6 +7,11 @@ moderator material.  SURVEY.md section 8 maps the BASELINE configs onto it:
 C1 = (12, 3, 100, 8), C3 (HM-small) = (34, 3, 11303, 100),
 C4 (HM-large) = (272, 3, 11303, 100).  ``analytic_infinite_medium`` has
 k_inf = nu*sigma_f/(sigma_c+sigma_f) = 1.215 in closed form.
+
+``shielding_slab`` is BASELINE config 5 (absent from the
+reference): a vacuum-bounded slab of alternating non-fissile layers (a
+light scatterer and two absorber mixes) driven by a surface source on z = 0,
+for fixed-source runs with a 3D mesh flux tally.
 """
 
 from __future__ import annotations
@@ -16,6 +21,12 @@ import numpy as np
 from .geometry import Pincell
 from .prng import STRIDE, skip_ahead
 from .xslib import Library, Material, NuclideXS, _make_composition, _make_nuclide
+
+# shielding slab (extension): per-material channel bands, densities
+SLAB_BANDS = (((3.0, 8.0), (0.05, 0.3)),      # light scatterer (scatter, capture barns)
+              ((2.0, 5.0), (0.2, 1.0)),       # absorber mix A
+              ((1.0, 4.0), (0.5, 2.0)))       # absorber mix B
+SLAB_DENSITY = (1.0e-3, 1.0e-2)
 
 DEFAULT_FUEL_NUCLIDES = 251
 DEFAULT_MODERATOR_NUCLIDES = 3
@@ -63,3 +74,29 @@ def analytic_infinite_medium() -> tuple[Library, Pincell]:
                     np.array([0.5, 0.5]), np.array([0.5, 0.5]), 2.43)
     library = Library([nuc], [Material(0, [(0, 1.0)])])
     return library, Pincell(n_axial=1, fuel_material_ids=[0], moderator_material_id=0)
+
+
+def shielding_slab(nuclides_per_material: int = 8, gridpoints: int = 2000, n_layers: int = 12,
+                   width: float = 60.0, thickness: float = 60.0,
+                   seed: int = 7) -> tuple[Library, Pincell]:
+    """Fixed-source shielding benchmark (BASELINE config 5): three synthetic
+    non-fissile materials (scatterer, two absorber mixes), ``n_layers`` layers
+    of equal thickness along z cycling scatterer/A/scatterer/B, a
+    ``width`` x ``width`` x ``thickness`` cm box with vacuum boundaries.
+    Run it with ``RunConfig(run_mode="fixed_source", mesh=(nx, ny, nz))``."""
+    nuclides, materials = [], []
+    for m, (sb, cb) in enumerate(SLAB_BANDS):
+        for i in range(nuclides_per_material):
+            k = m * nuclides_per_material + i
+            nuclides.append(_make_nuclide(skip_ahead(seed, k * STRIDE), gridpoints, sb, cb, (0.1, 0.2),
+                                          force_nonfissile=True))
+    n_total = len(nuclides)
+    for m in range(len(SLAB_BANDS)):
+        materials.append(Material(m, _make_composition(skip_ahead(seed, (n_total + m) * STRIDE),
+                                                       nuclides_per_material, nuclides_per_material,
+                                                       SLAB_DENSITY, id_offset=m * nuclides_per_material)))
+    library = Library(nuclides, materials, generation_seed=seed)
+    layers = [(0, 1, 0, 2)[j % 4] for j in range(n_layers)]
+    cell = Pincell(fuel_radius=0.0, pitch=width, height=thickness, n_axial=n_layers,
+                   fuel_material_ids=layers, moderator_material_id=0, boundary="vacuum")
+    return library, cell

@@ -44,6 +44,7 @@ _COUNTER_SUMS = (("captures", 5), ("fissions", 6), ("sourced", 7), ("energy_clam
                  ("invocations_advance", 16), ("invocations_collision", 17), ("sorts", 18))
 _COUNTER_MAXES = (("max_draws_per_history", 8), ("max_log_entries_per_history", 20),
                   ("max_in_flight_observed", 19))
+_COUNTER_LEAKS = (("leaks", 22),)          # extension: vacuum boundaries
 
 _ENGINES: dict[int, DeviceEngine] = {}
 
@@ -88,7 +89,10 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
         raise ConfigurationError("more ranks than particles per batch")
     g_lo, g_hi = block_of(world.rank, world.size, ppb)
     eng = engine_for(_local_device(world), library, pincell)
+    eng.set_extensions(pincell, config)
     eng.configure(config, g_lo, g_hi - g_lo)
+    fixed_source = config.run_mode == "fixed_source"
+    mesh = _MeshAccumulator(world, eng, config) if config.mesh is not None else None
 
     layout = TallyLayout(pincell.n_axial)
     use_logs = config.reduction == "deterministic"
@@ -143,14 +147,17 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
         batch_sums[b] = sums
         keff_values[b] = sums[layout.keff_bin] / weight
 
+        if mesh is not None and active:
+            mesh.add_batch()
         per_rank = allgather_array(world, out.counters)
         sourced = int(per_rank[:, 7].sum())
-        deaths = int(per_rank[:, 5].sum() + per_rank[:, 6].sum())
+        deaths = int(per_rank[:, 5].sum() + per_rank[:, 6].sum() + per_rank[:, 22].sum())
         if sourced != ppb or deaths != ppb:
             raise EventMCError(f"neutron bookkeeping broken in batch {b}: {sourced} sourced, "
-                               f"{deaths} absorbed, {ppb} expected")
-        batch_counters = combine_counters(per_rank, _COUNTER_SUMS, _COUNTER_MAXES)
-        for name, _ in _COUNTER_SUMS:
+                               f"{deaths} absorbed or leaked, {ppb} expected")
+        sums_spec = _COUNTER_SUMS + (_COUNTER_LEAKS if pincell.boundary == "vacuum" else ())
+        batch_counters = combine_counters(per_rank, sums_spec, _COUNTER_MAXES)
+        for name, _ in sums_spec:
             run_counters[name] = run_counters.get(name, 0) + batch_counters[name]
         for name, _ in _COUNTER_MAXES:
             run_counters[name] = max(run_counters.get(name, 0), batch_counters[name])
@@ -167,8 +174,11 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
         for key, i in (("lookup", 0), ("advance", 1), ("collision", 2), ("sort", 3)):
             timings[key] += float(tim[i])
 
-        # population control for the next batch (R:271-280)
-        if b < n_batches - 1:
+        # population control for the next batch (R:271-280); a fixed-source
+        # run samples its source afresh every batch (extension)
+        if b < n_batches - 1 and fixed_source:
+            pass
+        elif b < n_batches - 1:
             if n_bank == 0:
                 raise PopulationCollapseError(f"no fission sites banked in batch {b}")
             u, _ = prng.next_uniform(prng.batch_stream(config.seed, b))
@@ -211,6 +221,10 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
                      if config.inactive_batches > 0 and inactive_wall > 0.0 else None)
     active_rate = (config.active_batches * ppb / active_wall
                    if config.active_batches > 0 and active_wall > 0.0 else None)
+    if mesh is not None:
+        mesh_mean, mesh_stderr = mesh.result(config.active_batches, weight)
+    else:
+        mesh_mean = mesh_stderr = None
     timings["gpu_launches"] = launches
     timings["nuclide_lookups_active"] = nuclide_lookups_active
     timings.update(act)
@@ -220,7 +234,50 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
                      inactive_rate=inactive_rate, active_rate=active_rate,
                      counters=run_counters, config=config.echo(),
                      library_fingerprint=xslib.library_fingerprint(library),
-                     geometry_fingerprint=pincell.fingerprint())
+                     geometry_fingerprint=pincell.fingerprint(),
+                     mesh_mean=mesh_mean, mesh_stderr=mesh_stderr)
+
+
+class _MeshAccumulator:
+    """Per-batch mesh sums (device, float64) summed across ranks, then
+    accumulated as sum and sum of squares over active batches on the device
+    (torch as plumbing); mean / stderr per source particle at the end, like
+    tally.batch_statistics for the dense bins."""
+
+    def __init__(self, world: World, eng, config):
+        import torch
+        self.world, self.eng = world, eng
+        self.shape = tuple(int(v) for v in config.mesh)[::-1] + (2,)
+        ptr, n = eng.mesh_device()
+        self.view = device_view(ptr, n, "float64", eng.device)
+        self.sum = torch.zeros_like(self.view)
+        self.sq = torch.zeros_like(self.view)
+
+    def add_batch(self):
+        import torch
+        x = self.view.clone()
+        if self.world.distributed:
+            import torch.distributed as dist
+            if self.world.device_backend:
+                dist.all_reduce(x)
+            else:                                       # gloo (tests): through host memory
+                h = x.cpu()
+                dist.all_reduce(h)
+                x = h.to(x.device)
+        self.sum += x
+        self.sq += x * x
+        torch.cuda.synchronize(x.device)     # the next batch re-zeroes the buffer on the engine stream
+
+    def result(self, n_active: int, weight: float):
+        s = self.sum.cpu().numpy() / weight
+        q = self.sq.cpu().numpy() / (weight * weight)
+        mean = s / max(n_active, 1)
+        if n_active >= 2:
+            var = np.maximum(q / n_active - mean * mean, 0.0) * n_active / (n_active - 1)
+            err = np.sqrt(var / n_active)
+        else:
+            err = np.full_like(mean, np.nan)
+        return mean.reshape(self.shape), err.reshape(self.shape)
 
 
 def _host_to_device_bank(eng, cols):

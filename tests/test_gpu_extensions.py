@@ -1,0 +1,77 @@
+"""GPU parity for the SURVEY 8f row-1 extension (fixed-source shielding slab,
+vacuum boundaries, 3D track-length mesh tallies) against the oracle's
+restatement of the same extension (the reference has none of these:
+parity is pinned to oracle/, see tests/test_oracle_extensions.py)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_library
+from oracle import driver
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2403_12345_b200")
+
+
+def _oracle(cfg, lib, cell):
+    return driver.run(dict(cfg.__dict__, slab=cell.is_slab, vacuum=cell.boundary == "vacuum"),
+                      lib.arrays(), cell.as_tuple())
+
+
+@pytest.mark.parametrize("mode,energy", [("event", 0.0), ("history", 0.0), ("event", 2.0e6)])
+def test_slab_fixed_source_matches_oracle(mode, energy):
+    lib, cell = P.shielding_slab(gridpoints=150)
+    cfg = P.RunConfig(particles_per_batch=1500, inactive_batches=0, active_batches=3, mode=mode,
+                      run_mode="fixed_source", source_energy=energy, mesh=(3, 5, 12),
+                      reduction="deterministic", max_in_flight=400)
+    res = P.run_replicated(cfg, lib, cell)
+    ores = _oracle(cfg, lib, cell)
+    assert res.physics_fingerprint() == driver.fingerprint(ores)
+    for k in ("sourced", "captures", "fissions", "leaks", "events_lookup", "events_collision",
+              "max_draws_per_history", "interp_transport"):
+        assert res.counters[k] == ores["counters"][k], k
+    # atomics only reorder the per-cell sums of bit-identical segment scores
+    assert np.allclose(res.mesh_mean, ores["mesh_mean"], rtol=1e-12, atol=0)
+    assert res.mesh_stderr.shape == res.mesh_mean.shape
+
+
+def test_slab_large_population_fast_reduction():
+    lib, cell = P.shielding_slab()
+    cfg = P.RunConfig(particles_per_batch=200_000, inactive_batches=0, active_batches=2,
+                      run_mode="fixed_source", mesh=(20, 20, 60), reduction="fast",
+                      max_in_flight=200_000)
+    res = P.run_replicated(cfg, lib, cell)
+    ores = _oracle(cfg, lib, cell)
+    for k in ("sourced", "captures", "leaks", "events_lookup", "events_collision"):
+        assert res.counters[k] == ores["counters"][k], k
+    assert np.allclose(res.batch_sums, ores["batch_sums"], rtol=1e-10, atol=0)
+    assert np.allclose(res.mesh_mean, ores["mesh_mean"], rtol=1e-10, atol=1e-300)
+    flux = res.batch_sums[:, 0:5 * cell.n_axial:5].sum() / cfg.particles_per_batch / 2
+    assert np.isclose(res.mesh_mean[..., 0].sum(), flux, rtol=1e-10)
+
+
+def test_mesh_on_eigenvalue_run_keeps_reference_fingerprint(golden):
+    run = golden["runs"]["c1_event"]
+    pm = golden["problems"]["c1"]
+    cell = P.Pincell(n_axial=pm["n_axial"], fuel_material_ids=pm["fuel_material_ids"],
+                     moderator_material_id=pm["moderator_material_id"])
+    cfg = P.RunConfig(**dict(run["config"], mesh=(4, 4, 8)))
+    res = P.run_replicated(cfg, golden_library("c1"), cell)
+    assert res.physics_fingerprint() == run["fingerprint"]
+    act = cfg.inactive_batches
+    flux = res.batch_sums[act:, 0:5 * (pm["n_axial"] + 1):5].sum() / cfg.particles_per_batch
+    assert np.isclose(res.mesh_mean[..., 0].sum() * cfg.active_batches, flux, rtol=1e-11)
+
+
+def test_vacuum_pincell_eigenvalue_matches_oracle(golden):
+    pm = golden["problems"]["small"]
+    cell = P.Pincell(n_axial=pm["n_axial"], fuel_material_ids=pm["fuel_material_ids"],
+                     moderator_material_id=pm["moderator_material_id"], boundary="vacuum")
+    lib = golden_library("small")
+    cfg = P.RunConfig(particles_per_batch=3000, inactive_batches=1, active_batches=2, mode="event",
+                      reduction="deterministic", max_in_flight=700)
+    res = P.run_replicated(cfg, lib, cell)
+    ores = _oracle(cfg, lib, cell)
+    assert res.physics_fingerprint() == driver.fingerprint(ores)
+    assert res.counters["leaks"] == ores["counters"]["leaks"] > 0
