@@ -46,7 +46,20 @@ sys.path.insert(0, ROOT)
 METRIC = "particles/s (active batches), HM-large depleted fuel, at 1/2/4/8 B200"
 WORKLOAD = dict(workload="C4 HM-large depleted pincell: depleted_pincell(272,3,11303,100,seed=1)",
                 ppb_per_gpu=40_000_000, mode="event", reduction="fast", tally_mode="fused",
-                sort="on (mat, log E) every lookup sweep", seed=42)
+                sort="on (group, log E, mat) every lookup sweep", seed=42)
+# --workload c5: BASELINE configs[4] (SURVEY 8f row 1 extension)
+METRIC_C5 = "particles/s (active batches), fixed-source shielding slab with 3D mesh flux tallies"
+WORKLOAD_C5 = dict(workload="C5 shielding_slab(8 nuclides/material, 2000 points, 12 layers, 60x60x60 cm, "
+                            "vacuum), surface source, mesh 100x100x120 track-length (flux, total)",
+                   ppb_per_gpu=10_000_000, mode="event", reduction="fast", run_mode="fixed_source",
+                   mesh=(100, 100, 120), seed=42)
+
+
+def problem(args):
+    import paper_2403_12345_b200 as P
+    if args.workload == "c5":
+        return P.shielding_slab()
+    return P.depleted_pincell(272, 3, 11303, 100, seed=1)
 BYTES_PER_NUCLIDE_LOOKUP = 64
 TRAFFIC_PROFILE = "r1s2_lookup_traffic.json"
 
@@ -124,17 +137,17 @@ def init_dist():
     return rank, ws, local
 
 
-def cpu_baseline(lib, cell, threads: int, ppb_sample: int, batches=(1, 2)) -> dict:
+def cpu_baseline(lib, cell, threads: int, ppb_sample: int, batches=(1, 2), ext=None) -> dict:
     """The C oracle (restatement of the reference kernels, pinned bit-exact to
     it) on this host's cores, W workers like run_replicated."""
     from oracle import driver
     cfg = dict(particles_per_batch=ppb_sample, inactive_batches=batches[0],
                active_batches=batches[1], mode="event", max_in_flight=10000,
                tally_mode="fused", reduction="deterministic", sort_enabled=True,
-               sort_every_n=1, seed=42, workers=threads)
+               sort_every_n=1, seed=42, workers=threads, **(ext or {}))
     res = driver.run(cfg, lib.arrays(), cell.as_tuple(), workers=threads)
     return dict(value=res["active_rate"], unit="particles/s", cores=threads, kind="port",
-                sample=f"C4 library, {ppb_sample} particles/batch x ({batches[0]} inactive + "
+                sample=f"{'C5 slab' if ext else 'C4'} library, {ppb_sample} particles/batch x ({batches[0]} inactive + "
                        f"{batches[1]} active), event mode, {threads} worker threads, "
                        f"deterministic reduction (reference defaults)")
 
@@ -145,22 +158,24 @@ def run_reference(args):
     rank, ws, _ = init_dist()
     if rank != 0:
         return
-    from paper_2403_12345_b200.presets import depleted_pincell
-    lib, cell = depleted_pincell(272, 3, 11303, 100, seed=1)
+    lib, cell = problem(args)
+    c5 = args.workload == "c5"
     threads = os.cpu_count() or 1
-    ppb = args.ref_particles or 3000 * threads
+    ppb = args.ref_particles or (30000 if c5 else 3000) * threads
     from oracle import driver
+    ext = dict(run_mode="fixed_source", mesh=WORKLOAD_C5["mesh"], slab=True, vacuum=True) if c5 else {}
     cfg = dict(particles_per_batch=ppb, inactive_batches=args.warmup, active_batches=args.steps,
                mode="event", max_in_flight=10000, tally_mode="fused", reduction="deterministic",
-               sort_enabled=True, sort_every_n=1, seed=42, workers=threads)
+               sort_enabled=True, sort_every_n=1, seed=42, workers=threads, **ext)
     res = driver.run(cfg, lib.arrays(), cell.as_tuple(), workers=threads)
     v = res["active_rate"]
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "particles/s",
+    line = {"impl": "reference", "metric": METRIC_C5 if c5 else METRIC, "value": v, "unit": "particles/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * res["active_wall"] / max(args.steps, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": dict(WORKLOAD, reduction="deterministic (reference default)", ppb_sample=ppb,
+            "config": dict(WORKLOAD_C5 if c5 else WORKLOAD, reduction="deterministic (reference default)",
+                           ppb_sample=ppb,
                            impl="C restatement of the reference kernels (oracle/, bit-exact with the "
                                 "numba reference on this image's glibc)"),
             "cpu_baseline": {"value": v, "unit": "particles/s", "cores": threads, "kind": "port",
@@ -178,13 +193,15 @@ def run_ours(args):
     from paper_2403_12345_b200.distributed import current_world
 
     t0 = time.perf_counter()
-    lib, cell = P.depleted_pincell(272, 3, 11303, 100, seed=1)
+    lib, cell = problem(args)
     t_lib = time.perf_counter() - t0
-    ppb_gpu = args.particles
+    c5 = args.workload == "c5"
+    ppb_gpu = args.particles or (WORKLOAD_C5 if c5 else WORKLOAD)["ppb_per_gpu"]
+    ext = dict(run_mode="fixed_source", mesh=WORKLOAD_C5["mesh"]) if c5 else {}
     cfg = P.RunConfig(particles_per_batch=ppb_gpu * ws, inactive_batches=args.warmup,
                       active_batches=args.steps, mode="event", sort_enabled=True,
                       max_in_flight=args.max_in_flight or ppb_gpu, tally_mode="fused",
-                      reduction="fast", seed=42, workers=ws)
+                      reduction="fast", seed=42, workers=ws, **ext)
     dev = torch.cuda.current_device()
     eng = replication.engine_for(dev, lib, cell)
     stream = torch.cuda.current_stream()
@@ -235,11 +252,11 @@ def run_ours(args):
     except Exception:  # noqa: BLE001
         traffic = None
     line = {
-        "metric": METRIC, "value": value, "unit": "particles/s", "n_gpus": ws,
+        "metric": METRIC_C5 if c5 else METRIC, "value": value, "unit": "particles/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": dict(WORKLOAD, global_batch=cfg.particles_per_batch,
+        "config": dict(WORKLOAD_C5 if c5 else WORKLOAD, global_batch=cfg.particles_per_batch,
                        parallelism=f"domain replication x{ws}", l2="inputs >> L2 in traffic; no flush",
                        library_build_s=round(t_lib, 2)),
         "e2e": {"value": res.active_rate, "unit": "particles/s",
@@ -257,7 +274,13 @@ def run_ours(args):
     }
     if ws == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        line["cpu_baseline"] = cpu_baseline(lib, cell, threads, args.cpu_particles or 1000 * threads)
+        line["cpu_baseline"] = cpu_baseline(lib, cell, threads, args.cpu_particles or 1000 * threads,
+                                            ext=dict(ext, slab=cell.is_slab, vacuum=cell.boundary == "vacuum")
+                                            if c5 else None)
+    if c5:
+        line["mesh"] = {"cells": int(np.prod(WORKLOAD_C5["mesh"])),
+                        "flux_first_layer": float(res.mesh_mean[0, ..., 0].sum()),
+                        "leaks": res.counters.get("leaks")}
     print(json.dumps(line), flush=True)
 
 
@@ -267,7 +290,10 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--particles", type=int, default=40_000_000, help="particles per GPU per batch")
+    ap.add_argument("--particles", type=int, default=0,
+                    help="particles per GPU per batch (default 40M for c4, 10M for c5)")
+    ap.add_argument("--workload", default="c4", choices=("c4", "c5"),
+                    help="c4: headline HM-large eigenvalue (BASELINE metric); c5: fixed-source slab + mesh")
     ap.add_argument("--max-in-flight", type=int, default=0)
     ap.add_argument("--cpu-particles", type=int, default=0)
     ap.add_argument("--ref-particles", type=int, default=0)
