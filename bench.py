@@ -55,10 +55,19 @@ WORKLOAD_C5 = dict(workload="C5 shielding_slab(8 nuclides/material, 2000 points,
                    mesh=(100, 100, 120), seed=42)
 
 
+# --workload c2: BASELINE configs[1] (17x17 assembly, SURVEY 8f row 2 extension)
+METRIC_C2 = "particles/s (active batches), 2D 17x17 PWR assembly, ~30 nuclides"
+WORKLOAD_C2 = dict(workload="C2 pwr_assembly(27 fuel + 3 moderator nuclides, 11303 points, 17x17 lattice, "
+                            "25 water holes, 2D reflective), k-eigenvalue",
+                   ppb_per_gpu=1_000_000, mode="event", reduction="fast", seed=42)
+
+
 def problem(args):
     import paper_2403_12345_b200 as P
     if args.workload == "c5":
         return P.shielding_slab()
+    if args.workload == "c2":
+        return P.pwr_assembly()
     return P.depleted_pincell(272, 3, 11303, 100, seed=1)
 BYTES_PER_NUCLIDE_LOOKUP = 64
 TRAFFIC_PROFILE = "r1s2_lookup_traffic.json"
@@ -147,7 +156,8 @@ def cpu_baseline(lib, cell, threads: int, ppb_sample: int, batches=(1, 2), ext=N
                sort_every_n=1, seed=42, workers=threads, **(ext or {}))
     res = driver.run(cfg, lib.arrays(), cell.as_tuple(), workers=threads)
     return dict(value=res["active_rate"], unit="particles/s", cores=threads, kind="port",
-                sample=f"{'C5 slab' if ext else 'C4'} library, {ppb_sample} particles/batch x ({batches[0]} inactive + "
+                sample=f"{'C5 slab' if ext and 'mesh' in ext else ('C2 assembly' if ext else 'C4')} library, "
+                       f"{ppb_sample} particles/batch x ({batches[0]} inactive + "
                        f"{batches[1]} active), event mode, {threads} worker threads, "
                        f"deterministic reduction (reference defaults)")
 
@@ -164,17 +174,21 @@ def run_reference(args):
     ppb = args.ref_particles or (30000 if c5 else 3000) * threads
     from oracle import driver
     ext = dict(run_mode="fixed_source", mesh=WORKLOAD_C5["mesh"], slab=True, vacuum=True) if c5 else {}
+    if cell.lattice > 1:
+        ext["lattice"] = (cell.lattice, cell.pitch, cell.pin_map)
     cfg = dict(particles_per_batch=ppb, inactive_batches=args.warmup, active_batches=args.steps,
                mode="event", max_in_flight=10000, tally_mode="fused", reduction="deterministic",
                sort_enabled=True, sort_every_n=1, seed=42, workers=threads, **ext)
     res = driver.run(cfg, lib.arrays(), cell.as_tuple(), workers=threads)
     v = res["active_rate"]
-    line = {"impl": "reference", "metric": METRIC_C5 if c5 else METRIC, "value": v, "unit": "particles/s",
+    line = {"impl": "reference", "metric": {"c2": METRIC_C2, "c5": METRIC_C5}.get(args.workload, METRIC),
+            "value": v, "unit": "particles/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * res["active_wall"] / max(args.steps, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": dict(WORKLOAD_C5 if c5 else WORKLOAD, reduction="deterministic (reference default)",
+            "config": dict({"c2": WORKLOAD_C2, "c5": WORKLOAD_C5}.get(args.workload, WORKLOAD),
+                           reduction="deterministic (reference default)",
                            ppb_sample=ppb,
                            impl="C restatement of the reference kernels (oracle/, bit-exact with the "
                                 "numba reference on this image's glibc)"),
@@ -196,7 +210,8 @@ def run_ours(args):
     lib, cell = problem(args)
     t_lib = time.perf_counter() - t0
     c5 = args.workload == "c5"
-    ppb_gpu = args.particles or (WORKLOAD_C5 if c5 else WORKLOAD)["ppb_per_gpu"]
+    wl = {"c2": WORKLOAD_C2, "c5": WORKLOAD_C5}.get(args.workload, WORKLOAD)
+    ppb_gpu = args.particles or wl["ppb_per_gpu"]
     ext = dict(run_mode="fixed_source", mesh=WORKLOAD_C5["mesh"]) if c5 else {}
     cfg = P.RunConfig(particles_per_batch=ppb_gpu * ws, inactive_batches=args.warmup,
                       active_batches=args.steps, mode="event", sort_enabled=True,
@@ -252,11 +267,12 @@ def run_ours(args):
     except Exception:  # noqa: BLE001
         traffic = None
     line = {
-        "metric": METRIC_C5 if c5 else METRIC, "value": value, "unit": "particles/s", "n_gpus": ws,
+        "metric": {"c2": METRIC_C2, "c5": METRIC_C5}.get(args.workload, METRIC), "value": value,
+        "unit": "particles/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": dict(WORKLOAD_C5 if c5 else WORKLOAD, global_batch=cfg.particles_per_batch,
+        "config": dict(wl, global_batch=cfg.particles_per_batch,
                        parallelism=f"domain replication x{ws}", l2="inputs >> L2 in traffic; no flush",
                        library_build_s=round(t_lib, 2)),
         "e2e": {"value": res.active_rate, "unit": "particles/s",
@@ -274,9 +290,11 @@ def run_ours(args):
     }
     if ws == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
+        oext = dict(ext, slab=cell.is_slab, vacuum=cell.boundary == "vacuum") if c5 else {}
+        if cell.lattice > 1:
+            oext["lattice"] = (cell.lattice, cell.pitch, cell.pin_map)
         line["cpu_baseline"] = cpu_baseline(lib, cell, threads, args.cpu_particles or 1000 * threads,
-                                            ext=dict(ext, slab=cell.is_slab, vacuum=cell.boundary == "vacuum")
-                                            if c5 else None)
+                                            ext=oext or None)
     if c5:
         line["mesh"] = {"cells": int(np.prod(WORKLOAD_C5["mesh"])),
                         "flux_first_layer": float(res.mesh_mean[0, ..., 0].sum()),
@@ -292,8 +310,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--particles", type=int, default=0,
                     help="particles per GPU per batch (default 40M for c4, 10M for c5)")
-    ap.add_argument("--workload", default="c4", choices=("c4", "c5"),
-                    help="c4: headline HM-large eigenvalue (BASELINE metric); c5: fixed-source slab + mesh")
+    ap.add_argument("--workload", default="c4", choices=("c4", "c2", "c5"),
+                    help="c4: headline HM-large eigenvalue (BASELINE metric); c2: 17x17 assembly; "
+                         "c5: fixed-source slab + mesh")
     ap.add_argument("--max-in-flight", type=int, default=0)
     ap.add_argument("--cpu-particles", type=int, default=0)
     ap.add_argument("--ref-particles", type=int, default=0)

@@ -117,6 +117,12 @@ int emc_upload_geometry(emc_ctx *ctx, const emc_geometry *geom);
  *   mesh: nx*ny*nz track-length (flux, total rate) tally over the box, one
  *   batch's sums at emc_mesh_device() after each emc_run_batch (2 per cell). */
 int emc_set_geometry_options(emc_ctx *ctx, int32_t slab, int32_t vacuum);
+/* Lattice extension (BASELINE config 2): n x n pin cells of
+ * `pitch` filling the box (emc_geometry.half_pitch must be n*pitch/2);
+ * pin_map[j*n+i] != 0: fuel pin of `radius` with the axial fuel materials,
+ * 0: water hole.  Batch 0 samples a fuel pin uniformly, then its disk.
+ * n <= 1 restores the reference's single pincell. */
+int emc_set_lattice(emc_ctx *ctx, int32_t n, double pitch, const int32_t *pin_map);
 int emc_set_fixed_source(emc_ctx *ctx, int32_t enabled, double energy);
 int emc_set_mesh(emc_ctx *ctx, int32_t nx, int32_t ny, int32_t nz);
 int emc_mesh_device(emc_ctx *ctx, double **ptr, int64_t *n);

@@ -65,7 +65,9 @@ class OGeom(C.Structure):
                 ("slab", C.c_int32), ("vacuum", C.c_int32), ("mesh", P),
                 ("mnx", C.c_int32), ("mny", C.c_int32), ("mnz", C.c_int32), ("mpad", C.c_int32),
                 ("mx0", C.c_double), ("my0", C.c_double), ("mz0", C.c_double),
-                ("mdx", C.c_double), ("mdy", C.c_double), ("mdz", C.c_double)]
+                ("mdx", C.c_double), ("mdy", C.c_double), ("mdz", C.c_double),
+                ("lat_n", C.c_int32), ("n_pins", C.c_int32), ("pitch", C.c_double),
+                ("pin_map", P), ("pin_xy", P)]
 
 
 class OSlots(C.Structure):
@@ -166,9 +168,9 @@ class OracleGeometry:
     With a mesh, ``self.mesh`` is this geometry's accumulator (one per worker:
     see OracleGeometry.for_worker)."""
 
-    def __init__(self, geom, slab=False, vacuum=False, mesh=None):
+    def __init__(self, geom, slab=False, vacuum=False, mesh=None, lattice=None):
         radius, r2, hp, height, n_axial, zplanes, fuel_mats, mod_mat = geom
-        self.args = (geom, slab, vacuum, mesh)
+        self.args = (geom, slab, vacuum, mesh, lattice)
         self.keep = [np.ascontiguousarray(zplanes, np.float64),
                      np.ascontiguousarray(fuel_mats, np.int32)]
         self.n_axial = int(n_axial)
@@ -180,9 +182,17 @@ class OracleGeometry:
             box = (-hp, -hp, 0.0, (2.0 * hp) / nx, (2.0 * hp) / ny, height / nz)
         else:
             self.mesh, mptr, dims, box = None, None, (0, 0, 0, 0), (0.0,) * 6
+        lat = (1, 0, 0.0, None, None)
+        if lattice is not None and int(lattice[0]) > 1:     # (n, pitch, pin_map)
+            n, pitch, pmap = int(lattice[0]), float(lattice[1]), np.asarray(lattice[2], np.int32)
+            xy = [(-hp + (i + 0.5) * pitch, -hp + (j + 0.5) * pitch)
+                  for j in range(n) for i in range(n) if pmap[j * n + i]]
+            self.keep += [np.ascontiguousarray((pmap != 0).astype(np.int32)),
+                          np.ascontiguousarray(np.array(xy, np.float64).ravel())]
+            lat = (n, len(xy), pitch, _p(self.keep[2]), _p(self.keep[3]))
         self.s = OGeom(float(radius), float(r2), hp, height,
                        int(n_axial), _p(self.keep[0]), _p(self.keep[1]),
-                       int(mod_mat), int(bool(slab)), int(bool(vacuum)), mptr, *dims, *box)
+                       int(mod_mat), int(bool(slab)), int(bool(vacuum)), mptr, *dims, *box, *lat)
 
     def for_worker(self):
         return OracleGeometry(*self.args) if self.mesh is not None else self
@@ -345,7 +355,7 @@ def run(cfg: dict, lib_arrays, geom, workers: int | None = None,
     olib = OracleLibrary(lib_arrays)
     mesh = cfg.get("mesh")
     ogeom = OracleGeometry(geom, slab=cfg.get("slab", False), vacuum=cfg.get("vacuum", False),
-                           mesh=mesh)
+                           mesh=mesh, lattice=cfg.get("lattice"))
     fixed = cfg.get("run_mode", "eigenvalue") == "fixed_source"
     ppb = int(cfg["particles_per_batch"])
     n_axial = ogeom.n_axial

@@ -29,7 +29,8 @@
 #define NUDGE 1e-9
 #define MAX_HIST_LOG 100000
 
-enum { SURF_CYL = 0, SURF_XMIN, SURF_XMAX, SURF_YMIN, SURF_YMAX, SURF_ZMIN, SURF_ZMAX, SURF_AXIAL_BASE };
+enum { SURF_CYL = 0, SURF_XMIN, SURF_XMAX, SURF_YMIN, SURF_YMAX, SURF_ZMIN, SURF_ZMAX, SURF_AXIAL_BASE,
+       SURF_LATTICE = 30000 /* extension: internal lattice cell plane */ };
 enum { KIND_FUEL = 0, KIND_MOD = 1 };
 enum { ROUTE_ERROR = -1, ROUTE_COLLISION = 0, ROUTE_LOOKUP = 1, ROUTE_LEAK = 2, OUT_SCATTER = 0, OUT_DIED = 1 };
 enum { CNT_LOG_N = 0, CNT_SITE_N, CNT_OVF, CNT_ERR, CNT_ERR_AUX, CNT_CAPTURES, CNT_FISSIONS,
@@ -57,6 +58,8 @@ typedef struct {
     int32_t slab, vacuum;
     double *mesh; int32_t mnx, mny, mnz, mpad;
     double mx0, my0, mz0, mdx, mdy, mdz;
+    /* lattice extension: lat_n x lat_n pin cells of pitch */
+    int32_t lat_n, n_pins; double pitch; const int32_t *pin_map; const double *pin_xy;
 } OGeom;
 
 typedef struct {
@@ -116,10 +119,35 @@ static inline int64_t axial_index(double z, int64_t n_axial, double height) {
     if (a < 0) a = 0; else if (a > n_axial - 1) a = n_axial - 1;
     return a;
 }
+/* lattice extension: cell of a point, its centre and planes (same
+ * operation order as csrc/emc_device.cuh lattice_cell / lattice_lo / _hi) */
+static void lattice_cell(const OGeom *g, double x, double y, int32_t *i, int32_t *j, double *cx, double *cy) {
+    int32_t a = (int32_t)floor((x + g->hp) / g->pitch), b = (int32_t)floor((y + g->hp) / g->pitch);
+    a = a < 0 ? 0 : (a > g->lat_n - 1 ? g->lat_n - 1 : a);
+    b = b < 0 ? 0 : (b > g->lat_n - 1 ? g->lat_n - 1 : b);
+    *i = a; *j = b;
+    *cx = -g->hp + ((double)a + 0.5) * g->pitch;
+    *cy = -g->hp + ((double)b + 0.5) * g->pitch;
+}
+static double lattice_lo(const OGeom *g, int32_t i) { return i == 0 ? -g->hp : -g->hp + (double)i * g->pitch; }
+static double lattice_hi(const OGeom *g, int32_t i) {
+    return i == g->lat_n - 1 ? g->hp : -g->hp + (double)(i + 1) * g->pitch;
+}
+
 /* K:403-415 */
 void oracle_locate(double x, double y, double z, const OGeom *g, int64_t *out3) {
     if (x < -g->hp || x > g->hp || y < -g->hp || y > g->hp || z < 0.0 || z > g->height) {
         out3[0] = out3[1] = out3[2] = -1; return;
+    }
+    if (g->lat_n > 1) {
+        int32_t i, j; double cx, cy;
+        lattice_cell(g, x, y, &i, &j, &cx, &cy);
+        double xl = x - cx, yl = y - cy;
+        if (g->pin_map[j * g->lat_n + i] && xl * xl + yl * yl < g->r2) {
+            int64_t a = axial_index(z, g->n_axial, g->height);
+            out3[0] = KIND_FUEL; out3[1] = a; out3[2] = g->fuel_mats[a]; return;
+        }
+        out3[0] = KIND_MOD; out3[1] = -1; out3[2] = g->mod_mat; return;
     }
     if (g->slab || x * x + y * y < g->r2) {
         int64_t a = axial_index(z, g->n_axial, g->height);
@@ -132,6 +160,40 @@ double oracle_boundary_distance(double x, double y, double z, double ux, double 
                                 int64_t kd, int64_t ax, const OGeom *g, int64_t *surf_out) {
     double best = INFINITY, t; int64_t surf = -1;
     double a = ux * ux + uy * uy;
+    if (g->lat_n > 1) {          /* lattice extension */
+        int32_t li, lj; double cx, cy;
+        lattice_cell(g, x, y, &li, &lj, &cx, &cy);
+        double xl = x - cx, yl = y - cy;
+        int pin = g->pin_map[lj * g->lat_n + li] != 0;
+        if (kd == KIND_FUEL) {
+            if (a > 0.0) {
+                double b = 2.0 * (xl * ux + yl * uy), c = xl * xl + yl * yl - g->r2;
+                double disc = b * b - 4.0 * a * c;
+                if (disc > 0.0) { t = (-b + sqrt(disc)) / (2.0 * a); if (t > DIST_EPS && t < best) { best = t; surf = SURF_CYL; } }
+            }
+            if (uz > 0.0) {
+                t = (g->zplanes[ax + 1] - z) / uz;
+                if (t > DIST_EPS && t < best) { best = t; surf = ax == g->n_axial - 1 ? SURF_ZMAX : SURF_AXIAL_BASE + ax + 1; }
+            } else if (uz < 0.0) {
+                t = (g->zplanes[ax] - z) / uz;
+                if (t > DIST_EPS && t < best) { best = t; surf = ax == 0 ? SURF_ZMIN : SURF_AXIAL_BASE + ax; }
+            }
+        } else {
+            if (pin && a > 0.0) {
+                double b = 2.0 * (xl * ux + yl * uy), c = xl * xl + yl * yl - g->r2;
+                double disc = b * b - 4.0 * a * c;
+                if (disc > 0.0) { t = (-b - sqrt(disc)) / (2.0 * a); if (t > DIST_EPS && t < best) { best = t; surf = SURF_CYL; } }
+            }
+            if (ux > 0.0) { t = (lattice_hi(g, li) - x) / ux; if (t > DIST_EPS && t < best) { best = t; surf = li == g->lat_n - 1 ? SURF_XMAX : SURF_LATTICE; } }
+            else if (ux < 0.0) { t = (lattice_lo(g, li) - x) / ux; if (t > DIST_EPS && t < best) { best = t; surf = li == 0 ? SURF_XMIN : SURF_LATTICE; } }
+            if (uy > 0.0) { t = (lattice_hi(g, lj) - y) / uy; if (t > DIST_EPS && t < best) { best = t; surf = lj == g->lat_n - 1 ? SURF_YMAX : SURF_LATTICE; } }
+            else if (uy < 0.0) { t = (lattice_lo(g, lj) - y) / uy; if (t > DIST_EPS && t < best) { best = t; surf = lj == 0 ? SURF_YMIN : SURF_LATTICE; } }
+            if (uz > 0.0) { t = (g->height - z) / uz; if (t > DIST_EPS && t < best) { best = t; surf = SURF_ZMAX; } }
+            else if (uz < 0.0) { t = (0.0 - z) / uz; if (t > DIST_EPS && t < best) { best = t; surf = SURF_ZMIN; } }
+        }
+        *surf_out = surf;
+        return best;
+    }
     if (kd == KIND_FUEL) {
         if (g->slab) {    /* extension: slab layer bounded by the box side planes */
             if (ux > 0.0) { t = (g->hp - x) / ux; if (t > DIST_EPS && t < best) { best = t; surf = SURF_XMAX; } }
@@ -371,7 +433,7 @@ static int op_advance(int64_t i, const OSlots *S, const OLib *L, const OGeom *G,
     if (surf == SURF_CYL) {
         if (S->kind[i] == KIND_FUEL) { S->kind[i] = KIND_MOD; S->axial[i] = -1; }
         else { S->kind[i] = KIND_FUEL; S->axial[i] = (int32_t)axial_index(S->pz[i], G->n_axial, G->height); }
-    } else if (surf >= SURF_AXIAL_BASE) {
+    } else if (surf >= SURF_AXIAL_BASE && surf < SURF_LATTICE) {
         int64_t jpl = surf - SURF_AXIAL_BASE;
         S->axial[i] = (int32_t)(S->dz[i] > 0.0 ? jpl : jpl - 1);
     }
@@ -472,13 +534,19 @@ static int op_source(int64_t i, int64_t g, const OSlots *S, const OLib *L, const
         if (P->src_energy > 0.0) S->en[i] = P->src_energy;
         else { double ue = draw(S, i); S->en[i] = clamp_energy(-P->fission_t * log(1.0 - ue), L, cnt); }
     } else if (P->batch0) {
-        double x, y;
+        double x, y, cx = 0.0, cy = 0.0;
+        if (G->lat_n > 1) {    /* lattice extension: uniform fuel pin, then its disk */
+            int64_t k = (int64_t)(draw(S, i) * (double)G->n_pins);
+            if (k > G->n_pins - 1) k = G->n_pins - 1;
+            cx = G->pin_xy[2 * k]; cy = G->pin_xy[2 * k + 1];
+        }
         for (;;) {
             double u1 = draw(S, i), u2 = draw(S, i);
             x = (2.0 * u1 - 1.0) * G->radius; y = (2.0 * u2 - 1.0) * G->radius;
             if (x * x + y * y < G->r2) break;
             if (S->draws[i] >= (int64_t)STRIDE) { cnt[CNT_ERR] = ERR_STREAM_OVERLAP; cnt[CNT_ERR_AUX] = g; return -1; }
         }
+        if (G->lat_n > 1) { x = cx + x; y = cy + y; }
         double z = draw(S, i) * G->height;
         double ua = draw(S, i), ub = draw(S, i), d3[3];
         oracle_isotropic(ua, ub, d3);

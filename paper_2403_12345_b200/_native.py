@@ -69,6 +69,7 @@ SYMBOLS = {
     "emc_configure": (C.c_int, [_P, C.POINTER(EmcRunConfig)]),
     "emc_set_geometry_options": (C.c_int, [_P, _I32, _I32]),
     "emc_set_fixed_source": (C.c_int, [_P, _I32, _D]),
+    "emc_set_lattice": (C.c_int, [_P, _I32, _D, _P]),
     "emc_set_mesh": (C.c_int, [_P, _I32, _I32, _I32]),
     "emc_mesh_device": (C.c_int, [_P, C.POINTER(_P), C.POINTER(_I64)]),
     "emc_set_source_local": (C.c_int, [_P, _D]),

@@ -120,6 +120,7 @@ struct emc_ctx {
     // geometry
     bool have_geom = false;
     DBuf<double> zplanes; DBuf<int32_t> fuel_mats;
+    DBuf<int32_t> pin_map; DBuf<double> pin_xy;
     DGeom G{};
 
     // extensions: fixed surface source, track-length mesh
@@ -172,6 +173,11 @@ struct emc_ctx {
     Ctl* ctl_host = nullptr;
     DSrc src{};
     cudaEvent_t ev[16]{};
+    // tail mode (EMC_TAIL_N, EMC_TAIL_K): queues below tail_n once the source is
+    // exhausted run tail_k iterations per host round trip, unsorted
+    int64_t tail_n = 262144;
+    int tail_k = 16;
+    cudaEvent_t evt[4 * 32]{};
     bool ev_init = false;
 };
 
@@ -196,6 +202,9 @@ extern "C" int emc_create(int device, emc_ctx** out)
     if (cudaMallocHost(&c->ctl_host, sizeof(Ctl)) != cudaSuccess) { delete c; g_err = "cudaMallocHost"; return EMC_E_CUDA; }
     if (c->ctl.alloc(1) || c->cnt.alloc(EMC_N_COUNTERS)) { delete c; return EMC_E_OOM; }
     for (auto& e : c->ev) cudaEventCreate(&e);
+    for (auto& e : c->evt) cudaEventCreate(&e);
+    if (const char* t = getenv("EMC_TAIL_N")) c->tail_n = std::max<int64_t>(0, atoll(t));
+    if (const char* t = getenv("EMC_TAIL_K")) c->tail_k = std::max(1, std::min(32, atoi(t)));
     c->ev_init = true;
     *out = c;
     return 0;
@@ -219,7 +228,10 @@ extern "C" void emc_destroy(emc_ctx* c)
     c->lg_gid.release(); c->cnt.release(); c->ctl.release();
     c->sites.release(); c->banks[0].release(); c->banks[1].release();
     if (c->ctl_host) cudaFreeHost(c->ctl_host);
-    if (c->ev_init) for (auto& e : c->ev) cudaEventDestroy(e);
+    if (c->ev_init) {
+        for (auto& e : c->ev) cudaEventDestroy(e);
+        for (auto& e : c->evt) cudaEventDestroy(e);
+    }
     delete c;
 }
 
@@ -393,7 +405,7 @@ extern "C" int emc_upload_geometry(emc_ctx* c, const emc_geometry* g)
     EMC_TRY_CUDA(cudaMemcpy(c->zplanes.p, g->zplanes, (g->n_axial + 1) * 8, cudaMemcpyHostToDevice));
     EMC_TRY_CUDA(cudaMemcpy(c->fuel_mats.p, g->fuel_mats, g->n_axial * 4, cudaMemcpyHostToDevice));
     c->G = DGeom{g->radius, g->r2, g->half_pitch, g->height, (int32_t)g->n_axial, (int32_t)g->mod_mat,
-                 c->zplanes.p, c->fuel_mats.p, 0, 0};
+                 c->zplanes.p, c->fuel_mats.p, 0, 0, 1, 0, 0.0, nullptr, nullptr};
     c->M.on = 0;
     c->n_bins = (int32_t)((g->n_axial + 1) * 5 + 1);
     c->kbin = c->n_bins - 1;
@@ -406,6 +418,33 @@ extern "C" int emc_set_geometry_options(emc_ctx* c, int32_t slab, int32_t vacuum
     if (!c || !c->have_geom) return fail_arg("emc_set_geometry_options: upload the geometry first");
     c->G.slab = slab ? 1 : 0;
     c->G.vacuum = vacuum ? 1 : 0;
+    return 0;
+}
+
+extern "C" int emc_set_lattice(emc_ctx* c, int32_t n, double pitch, const int32_t* pin_map)
+{
+    if (!c || !c->have_geom) return fail_arg("emc_set_lattice: upload the geometry first");
+    if (n <= 1) { c->G.lat_n = 1; c->G.n_pins = 0; return 0; }
+    if (!pin_map || !(pitch > 0.0)) return fail_arg("emc_set_lattice: bad arguments");
+    if (!(2.0 * c->G.radius < pitch)) return fail_arg("emc_set_lattice: pins must fit their cells");
+    if (std::fabs(n * pitch - 2.0 * c->G.hp) > 1e-12 * n * pitch)
+        return fail_arg("emc_set_lattice: the box half-width must be n*pitch/2");
+    std::vector<double> xy;
+    for (int32_t j = 0; j < n; ++j)
+        for (int32_t i = 0; i < n; ++i)
+            if (pin_map[j * n + i]) {     // centres exactly as lattice_cell() forms them
+                xy.push_back(-c->G.hp + ((double)i + 0.5) * pitch);
+                xy.push_back(-c->G.hp + ((double)j + 0.5) * pitch);
+            }
+    if (xy.empty()) return fail_arg("emc_set_lattice: no fuel pins");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    if (c->pin_map.alloc((int64_t)n * n) || c->pin_xy.alloc(xy.size())) return EMC_E_OOM;
+    std::vector<int32_t> pm(pin_map, pin_map + (int64_t)n * n);
+    for (auto& v : pm) v = v ? 1 : 0;
+    EMC_TRY_CUDA(cudaMemcpy(c->pin_map.p, pm.data(), pm.size() * 4, cudaMemcpyHostToDevice));
+    EMC_TRY_CUDA(cudaMemcpy(c->pin_xy.p, xy.data(), xy.size() * 8, cudaMemcpyHostToDevice));
+    c->G.lat_n = n; c->G.n_pins = (int32_t)(xy.size() / 2); c->G.pitch = pitch;
+    c->G.pin_map = c->pin_map.p; c->G.pin_xy = c->pin_xy.p;
     return 0;
 }
 
@@ -659,9 +698,48 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
         EMC_TRY_CUDA(cudaMemcpyAsync(c->ctl_host, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
         EMC_TRY_CUDA(cudaStreamSynchronize(st));
         int64_t nL = c->ctl_host->nL2;
-        int64_t look_inv = 0;
+        int64_t look_inv = 0, tail_blocks = 0;
         float ms;
         while (nL > 0 && c->ctl_host->err == 0) {
+            if (nL <= c->tail_n && c->ctl_host->cursor >= (unsigned long long)cf.n_assigned) {
+                // tail mode: tail_k iterations back to back, queue lengths on the device
+                const int K = c->tail_k;
+                const unsigned gl = grid_for(nL, BLK, maxb);
+                for (int k = 0; k < K; ++k) {
+                    k_tail_begin<<<1, 1, 0, st>>>(c->ctl.p, c->cnt.p);
+                    EMC_CHECK_LAUNCH(c);
+                    EMC_TRY_CUDA(cudaEventRecord(c->evt[4 * k], st));
+                    EMC_TRY_CUDA(lk_launch<0>(c->lk_cfg, c->L, cur, nL, c->S, cf.fused, c->cnt.p, nullptr, nullptr,
+                                              nullptr, c->sm_count, c->lk_smem, st, &c->ctl.p->nLcur));
+                    c->launches += 1;
+                    EMC_TRY_CUDA(cudaEventRecord(c->evt[4 * k + 1], st));
+                    k_advance<<<gl, BLK, 0, st>>>(cur, (int32_t)nL, bp, c->L, c->G, c->S, lg, c->bins.p, c->qc.p,
+                                                  c->qx.p, c->ctl.p, c->cnt.p, c->M, &c->ctl.p->nLcur);
+                    EMC_CHECK_LAUNCH(c);
+                    k_crossing<<<gl, BLK, 0, st>>>(c->qx.p, &c->ctl.p->nX, bp, c->L, c->G, c->src, c->S, nxt,
+                                                   c->ctl.p, c->cnt.p);
+                    EMC_CHECK_LAUNCH(c);
+                    EMC_TRY_CUDA(cudaEventRecord(c->evt[4 * k + 2], st));
+                    k_collision<<<gl, BLK, 0, st>>>(c->qc.p, &c->ctl.p->nC, bp, c->L, c->G, c->src, c->S, lg, sv,
+                                                    c->bins.p, nxt, c->ctl.p, c->cnt.p);
+                    EMC_CHECK_LAUNCH(c);
+                    k_tail_end<<<1, 1, 0, st>>>(c->ctl.p, c->cnt.p);
+                    EMC_CHECK_LAUNCH(c);
+                    EMC_TRY_CUDA(cudaEventRecord(c->evt[4 * k + 3], st));
+                    std::swap(cur, nxt);
+                }
+                EMC_TRY_CUDA(cudaMemcpyAsync(c->ctl_host, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+                EMC_TRY_CUDA(cudaStreamSynchronize(st));
+                for (int k = 0; k < K; ++k) {
+                    cudaEventElapsedTime(&ms, c->evt[4 * k], c->evt[4 * k + 1]); tm[0] += ms * 1e-3;
+                    cudaEventElapsedTime(&ms, c->evt[4 * k + 1], c->evt[4 * k + 2]); tm[1] += ms * 1e-3;
+                    cudaEventElapsedTime(&ms, c->evt[4 * k + 2], c->evt[4 * k + 3]); tm[2] += ms * 1e-3;
+                }
+                iterations += K;
+                tail_blocks++;
+                nL = c->ctl_host->nL2;
+                continue;
+            }
             const int32_t* q = cur;
             EMC_TRY_CUDA(cudaMemsetAsync(&c->ctl.p->nL2, 0, 3 * sizeof(unsigned), st));
             bool do_sort = cf.sort_enabled && nL > 1 && (look_inv % cf.sort_every) == 0;
@@ -710,7 +788,7 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             EMC_CHECK_LAUNCH(c);
             EMC_TRY_CUDA(cudaEventRecord(c->ev[2], st));
             k_advance<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(q, (int32_t)nL, bp, c->L, c->G, c->S, lg, c->bins.p,
-                                                              c->qc.p, c->qx.p, c->ctl.p, c->cnt.p, c->M);
+                                                              c->qc.p, c->qx.p, c->ctl.p, c->cnt.p, c->M, nullptr);
             EMC_CHECK_LAUNCH(c);
             k_crossing<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(c->qx.p, &c->ctl.p->nX, bp, c->L, c->G, c->src, c->S,
                                                                nxt, c->ctl.p, c->cnt.p);

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(128) k_history(BatchP bp, DLib L, DGeom G, DSr
                 if (surf == SURF_CYL) {
                     if (kd == KIND_FUEL) { kd = KIND_MOD; ax = -1; }
                     else { kd = KIND_FUEL; ax = axial_index(z, G.n_axial, G.height); }
-                } else if (surf >= SURF_AXIAL_BASE) {
+                } else if (surf >= SURF_AXIAL_BASE && surf < SURF_LATTICE) {
                     int32_t jpl = surf - SURF_AXIAL_BASE;
                     ax = dz > 0.0 ? jpl : jpl - 1;
                 }

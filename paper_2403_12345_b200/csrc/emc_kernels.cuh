@@ -75,7 +75,12 @@ __device__ __forceinline__ bool source_particle(int32_t slot, int64_t g, const B
             a.E = clamp_energy(__dmul_rn(-bp.fission_t, emc_log(__dsub_rn(1.0, ue))), L, clamps);
         }
     } else if (bp.batch0) {
-        double x, y;
+        double x, y, cx = 0.0, cy = 0.0;
+        if (G.lat_n > 1) {       // lattice extension: uniform over the fuel pins, then the pin's disk
+            int64_t k = (int64_t)__dmul_rn(draw(s, draws), (double)G.n_pins);
+            k = k > G.n_pins - 1 ? G.n_pins - 1 : k;
+            cx = G.pin_xy[2 * k]; cy = G.pin_xy[2 * k + 1];
+        }
         for (;;) {
             double u1 = draw(s, draws), u2 = draw(s, draws);
             x = __dmul_rn(__dsub_rn(__dmul_rn(2.0, u1), 1.0), G.radius);
@@ -83,6 +88,7 @@ __device__ __forceinline__ bool source_particle(int32_t slot, int64_t g, const B
             if (__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)) < G.r2) break;
             if (draws >= kStride) { set_error(ctl, nullptr, ERR_STREAM_OVERLAP, g); return false; }
         }
+        if (G.lat_n > 1) { x = __dadd_rn(cx, x); y = __dadd_rn(cy, y); }
         a.x = x; a.y = y;
         a.z = __dmul_rn(draw(s, draws), G.height);
         double ua = draw(s, draws), ub = draw(s, draws);
@@ -311,8 +317,9 @@ __device__ __forceinline__ void score_bins(double* bins, bool valid, int32_t bas
 __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __restrict__ q, int32_t n, BatchP bp,
                                                  DLib L, DGeom G, DSlots S, DLog lg, double* bins,
                                                  int32_t* q_col, int32_t* q_cross, Ctl* ctl,
-                                                 unsigned long long* cnt, DMesh M)
+                                                 unsigned long long* cnt, DMesh M, const unsigned int* nptr)
 {
+    if (nptr) n = (int32_t)*nptr;        // tail mode: queue length lives on the device
     unsigned long long interp_score = 0;
     EMC_WARP_LOOP(n) {
         int64_t i = emc_base_ + lane_id();
@@ -451,7 +458,7 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_crossing(const int32_t* _
                 if (surf == SURF_CYL) {
                     if (d.kind == KIND_FUEL) { d.kind = KIND_MOD; d.axial = -1; }
                     else { d.kind = KIND_FUEL; d.axial = axial_index(a.z, G.n_axial, G.height); }
-                } else if (surf >= SURF_AXIAL_BASE) {
+                } else if (surf >= SURF_AXIAL_BASE && surf < SURF_LATTICE) {
                     int32_t jpl = surf - SURF_AXIAL_BASE;
                     d.axial = b.dz > 0.0 ? jpl : jpl - 1;
                 }
@@ -665,6 +672,31 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_collision(const int32_t* 
     warp_add_u64(cnt + CNT_CLAMPS, (unsigned long long)clamps);
     warp_max_u64(cnt + CNT_MAX_DRAWS, maxdraws);
     warp_max_u64(cnt + CNT_MAX_HIST_LOG, maxhist);
+}
+
+}  // namespace emc
+
+namespace emc {
+
+// Tail mode (small queues, source exhausted): iterations run back to back
+// without a host round trip.  Between iterations this one-thread kernel makes
+// the queue pushed by the last crossing/collision sweeps the current one and
+// keeps the event counters the host loop would have kept (K:1132-1206 counts).
+__global__ void k_tail_begin(Ctl* ctl, unsigned long long* cnt)
+{
+    const unsigned int n = ctl->nL2;
+    ctl->nLcur = n;
+    ctl->nL2 = 0; ctl->nC = 0; ctl->nX = 0;
+    if (n) {
+        cnt[CNT_EV_LOOKUP] += n; cnt[CNT_EV_ADVANCE] += n;
+        cnt[CNT_INV_LOOKUP] += 1; cnt[CNT_INV_ADVANCE] += 1;
+    }
+}
+
+__global__ void k_tail_end(Ctl* ctl, unsigned long long* cnt)
+{
+    const unsigned int c = ctl->nC;
+    if (c) { cnt[CNT_EV_COLLISION] += c; cnt[CNT_INV_COLLISION] += 1; }
 }
 
 }  // namespace emc

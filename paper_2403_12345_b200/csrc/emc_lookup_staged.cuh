@@ -207,8 +207,9 @@ template <int MODE, bool DEN_ST, int NW, int MINB>
 __global__ void __launch_bounds__(NW * 32, MINB)
     k_lookup_staged(const int32_t* __restrict__ q, int32_t n, DLib L, DSlots S, int32_t fused,
                     unsigned long long* cnt, const double* __restrict__ bE, const int32_t* __restrict__ bM,
-                    double* __restrict__ bout)
+                    double* __restrict__ bout, const unsigned int* nptr)
 {
+    if (nptr) n = (int32_t)*nptr;        // tail mode: queue length lives on the device
     extern __shared__ __align__(128) unsigned char lk_raw[];
     LkShared& sh = *reinterpret_cast<LkShared*>(lk_raw);
     double* const sden = reinterpret_cast<double*>(lk_raw + sizeof(LkShared));
@@ -394,27 +395,29 @@ constexpr int lk_cfg_minb(int c) { return c == 0 ? 1 : 2; }
 template <int MODE, int CFG>
 inline cudaError_t lk_launch_cfg(const DLib& L, const int32_t* q, int64_t n, DSlots S, int32_t fused,
                                  unsigned long long* cnt, const double* bE, const int32_t* bM, double* bout,
-                                 int sm_count, size_t smem, cudaStream_t st)
+                                 int sm_count, size_t smem, cudaStream_t st, const unsigned int* nptr)
 {
     constexpr int NW = lk_cfg_warps(CFG), MB = lk_cfg_minb(CFG);
     constexpr int64_t chunk = (NW - 1) * 32;
     const unsigned nb = (unsigned)std::min<int64_t>((n + chunk - 1) / chunk, (int64_t)sm_count * MB);
     if (L.den_staged)
-        k_lookup_staged<MODE, true, NW, MB><<<nb, NW * 32, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM, bout);
+        k_lookup_staged<MODE, true, NW, MB><<<nb, NW * 32, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM, bout,
+                                                                       nptr);
     else
-        k_lookup_staged<MODE, false, NW, MB><<<nb, NW * 32, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM, bout);
+        k_lookup_staged<MODE, false, NW, MB><<<nb, NW * 32, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM,
+                                                                        bout, nptr);
     return cudaGetLastError();
 }
 
 template <int MODE>
 inline cudaError_t lk_launch(int cfg, const DLib& L, const int32_t* q, int64_t n, DSlots S, int32_t fused,
                              unsigned long long* cnt, const double* bE, const int32_t* bM, double* bout, int sm_count,
-                             size_t smem, cudaStream_t st)
+                             size_t smem, cudaStream_t st, const unsigned int* nptr = nullptr)
 {
     switch (cfg) {
-    case 1: return lk_launch_cfg<MODE, 1>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st);
-    case 2: return lk_launch_cfg<MODE, 2>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st);
-    default: return lk_launch_cfg<MODE, 0>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st);
+    case 1: return lk_launch_cfg<MODE, 1>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, nptr);
+    case 2: return lk_launch_cfg<MODE, 2>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, nptr);
+    default: return lk_launch_cfg<MODE, 0>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, nptr);
     }
 }
 

@@ -113,6 +113,9 @@ class DeviceEngine:
                 "emc_set_geometry_options")
         N.check(self.lib.emc_set_fixed_source(self._h, int(config.run_mode == "fixed_source"),
                                               float(config.source_energy)), "emc_set_fixed_source")
+        n = int(getattr(pincell, "lattice", 1))
+        pm = np.ascontiguousarray(pincell.pin_map if n > 1 else [1], np.int32)
+        N.check(self.lib.emc_set_lattice(self._h, n, float(pincell.pitch), N.ptr(pm)), "emc_set_lattice")
         nx, ny, nz = (int(v) for v in config.mesh) if config.mesh is not None else (0, 0, 0)
         N.check(self.lib.emc_set_mesh(self._h, nx, ny, nz), "emc_set_mesh")
 

@@ -8,6 +8,10 @@ C1 = (12, 3, 100, 8), C3 (HM-small) = (34, 3, 11303, 100),
 C4 (HM-large) = (272, 3, 11303, 100).  ``analytic_infinite_medium`` has
 k_inf = nu*sigma_f/(sigma_c+sigma_f) = 1.215 in closed form.
 
+``pwr_assembly`` is BASELINE config 2 (absent from the
+reference): a 2D 17x17 lattice of depleted-fuel pins with 25 water holes
+(guide and instrument tube positions), ~30 synthetic nuclides, reflective.
+
 ``shielding_slab`` is BASELINE config 5 (absent from the
 reference): a vacuum-bounded slab of alternating non-fissile layers (a
 light scatterer and two absorber mixes) driven by a surface source on z = 0,
@@ -99,4 +103,25 @@ def shielding_slab(nuclides_per_material: int = 8, gridpoints: int = 2000, n_lay
     layers = [(0, 1, 0, 2)[j % 4] for j in range(n_layers)]
     cell = Pincell(fuel_radius=0.0, pitch=width, height=thickness, n_axial=n_layers,
                    fuel_material_ids=layers, moderator_material_id=0, boundary="vacuum")
+    return library, cell
+
+
+# 17x17 PWR assembly: guide-tube and central instrument-tube positions (row, column)
+PWR_17_WATER_HOLES = ((2, 5), (2, 8), (2, 11), (3, 3), (3, 13), (5, 2), (5, 5), (5, 8), (5, 11), (5, 14),
+                      (8, 2), (8, 5), (8, 8), (8, 11), (8, 14), (11, 2), (11, 5), (11, 8), (11, 11),
+                      (11, 14), (13, 3), (13, 13), (14, 5), (14, 8), (14, 11))
+
+
+def pwr_assembly(n_fuel_nuclides: int = 27, n_moderator_nuclides: int = 3, gridpoints: int = 11303,
+                 n_axial: int = 1, seed: int = 1) -> tuple[Library, Pincell]:
+    """BASELINE config 2: 17x17 fuel assembly (264 pins + 25 water holes) of
+    the depleted_pincell materials (same generator and seeds), reflective
+    outer planes; n_axial = 1 makes it 2D (reflective z planes)."""
+    library, pin = depleted_pincell(n_fuel_nuclides, n_moderator_nuclides, gridpoints, n_axial, seed)
+    pin_map = [1] * (17 * 17)
+    for r, c in PWR_17_WATER_HOLES:
+        pin_map[r * 17 + c] = 0
+    cell = Pincell(fuel_radius=pin.fuel_radius, pitch=pin.pitch, height=pin.height, n_axial=n_axial,
+                   fuel_material_ids=list(pin.fuel_material_ids),
+                   moderator_material_id=pin.moderator_material_id, lattice=17, pin_map=pin_map)
     return library, cell

@@ -75,3 +75,36 @@ def test_vacuum_pincell_eigenvalue_matches_oracle(golden):
     ores = _oracle(cfg, lib, cell)
     assert res.physics_fingerprint() == driver.fingerprint(ores)
     assert res.counters["leaks"] == ores["counters"]["leaks"] > 0
+
+
+@pytest.mark.parametrize("mode", ["event", "history"])
+def test_pwr_assembly_lattice_matches_oracle(mode):
+    """BASELINE config 2 geometry (17x17 lattice with water holes, SURVEY 8f
+    row 2) at parity scale: histories bit-identical to the oracle."""
+    lib, cell = P.pwr_assembly(gridpoints=300)
+    cfg = P.RunConfig(particles_per_batch=4000, inactive_batches=1, active_batches=2, mode=mode,
+                      reduction="deterministic", max_in_flight=1500, mesh=(17, 17, 1))
+    res = P.run_replicated(cfg, lib, cell)
+    ores = driver.run(dict(cfg.__dict__, lattice=(cell.lattice, cell.pitch, cell.pin_map)),
+                      lib.arrays(), cell.as_tuple())
+    assert res.physics_fingerprint() == driver.fingerprint(ores)
+    for k in ("sourced", "captures", "fissions", "events_lookup", "events_collision", "interp_transport"):
+        assert res.counters[k] == ores["counters"][k], k
+    assert np.allclose(res.mesh_mean, ores["mesh_mean"], rtol=1e-12, atol=0)
+
+
+def test_pwr_assembly_c2_scale_staged_equals_plain():
+    """C2 at 1M particles: the staged lookup and the plain kernel agree bit
+    for bit on the lattice problem (27-nuclide fuel group: staged path)."""
+    import os
+    lib, cell = P.pwr_assembly()
+    cfg = P.RunConfig(particles_per_batch=1_000_000, inactive_batches=1, active_batches=1,
+                      reduction="deterministic", max_in_flight=1_000_000)
+    out = {}
+    for kern in ("staged", "plain"):
+        os.environ["EMC_LOOKUP"] = kern
+        try:
+            out[kern] = P.run_replicated(cfg, lib, cell).physics_fingerprint()
+        finally:
+            os.environ.pop("EMC_LOOKUP", None)
+    assert out["staged"] == out["plain"]

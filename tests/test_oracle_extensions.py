@@ -75,3 +75,38 @@ def test_vacuum_pincell_leaks_and_balances(golden):
     c = res["counters"]
     assert c["leaks"] > 0
     assert c["captures"] + c["fissions"] + c["leaks"] == c["sourced"]
+
+
+# ---- lattice extension (BASELINE config 2) -------------------
+
+def _lattice_cfg(cell, **kw):
+    return dict(kw, lattice=(cell.lattice, cell.pitch, cell.pin_map))
+
+
+def test_full_lattice_equals_infinite_pincell_statistically():
+    """An all-pin reflective lattice is the same infinite medium as one
+    reflective pincell: k agrees within statistics (the histories differ)."""
+    lib, pin = P.depleted_pincell(12, 3, 100, 1, seed=1)
+    lat = P.Pincell(fuel_radius=pin.fuel_radius, pitch=pin.pitch, height=pin.height, n_axial=1,
+                    fuel_material_ids=pin.fuel_material_ids,
+                    moderator_material_id=pin.moderator_material_id, lattice=5)
+    base = dict(particles_per_batch=20000, inactive_batches=3, active_batches=10, mode="event",
+                reduction="fast", workers=8)
+    a = driver.run(dict(base), lib.arrays(), pin.as_tuple())
+    b = driver.run(_lattice_cfg(lat, **base), lib.arrays(), lat.as_tuple())
+    ka, kb = a["keff"][3:], b["keff"][3:]
+    se = np.sqrt(ka.var(ddof=1) / ka.size + kb.var(ddof=1) / kb.size)
+    assert abs(ka.mean() - kb.mean()) < 4.0 * se, (ka.mean(), kb.mean(), se)
+
+
+def test_assembly_mesh_is_pinwise_and_balanced():
+    lib, cell = P.pwr_assembly(gridpoints=200)
+    cfg = _lattice_cfg(cell, particles_per_batch=4000, inactive_batches=1, active_batches=2,
+                       mode="history", mesh=(17, 17, 1), reduction="deterministic")
+    res = driver.run(cfg, lib.arrays(), cell.as_tuple())
+    c = res["counters"]
+    assert c["captures"] + c["fissions"] == c["sourced"]
+    flux = res["batch_sums"][1:, 0:10:5].sum()
+    assert np.isclose(res["mesh_sum"][..., 0].sum(), flux, rtol=1e-12, atol=0)
+    ev = driver.run(dict(cfg, mode="event"), lib.arrays(), cell.as_tuple())
+    assert driver.fingerprint(ev) == driver.fingerprint(res)       # executor-invariant
