@@ -43,9 +43,17 @@ struct __align__(16) LkMeta {
     int32_t g0, hrow;              // global fallback
 };
 
+// fast-path meta word: window size (bits 0-4), mode (5-6), window starts at
+// the nuclide's first point (7)
+__host__ __device__ constexpr uint32_t lk_word(int32_t cnt, int32_t mode, int32_t lo)
+{
+    return (uint32_t)(cnt & 31) | ((uint32_t)mode << 5) | ((uint32_t)(lo == 0) << 7);
+}
+
 struct __align__(128) LkShared {
     unsigned long long full[LK_D], empty[LK_D];
     int32_t grp, bmin, bmax, pad;
+    uint32_t word[LK_D][LK_G];
     LkMeta meta[LK_D][LK_G];
     IvRec iv[LK_D][LK_G][LK_R];
 };
@@ -132,16 +140,15 @@ __global__ void k_build_intervals(const Rec* __restrict__ rec, const int64_t* __
     for (int64_t i = a + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < b; i += (int64_t)gridDim.x * blockDim.x) {
         const Rec p = rec[i];
         IvRec v;
-        v.E0 = p.E; v.t0 = p.t; v.c0 = p.c; v.f0 = p.f; v.pad = 0.0;
+        v.E0 = p.E; v.t0 = p.t; v.c0 = p.c; v.f0 = p.f;
         if (i + 1 < b) {
             const Rec q = rec[i + 1];
-            v.d = __dsub_rn(q.E, p.E);
-            v.r = div_rcp(v.d);
+            v.r = div_rcp(__dsub_rn(q.E, p.E));
             v.dt = __dsub_rn(q.t, p.t);
             v.dc = __dsub_rn(q.c, p.c);
             v.df = __dsub_rn(q.f, p.f);
         } else {
-            v.d = 0.0; v.r = 0.0; v.dt = 0.0; v.dc = 0.0; v.df = 0.0;
+            v.r = 0.0; v.dt = 0.0; v.dc = 0.0; v.df = 0.0;
         }
         iv[i] = v;
     }
@@ -288,7 +295,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                     if (T >= (uint32_t)LK_D) mbar_wait(&sh.empty[d], ((T / LK_D) - 1) & 1);
                     uint32_t bytes = 0;
                     const bool copy_iv = lane < LK_G && cur.valid && cur.mt.mode != LK_GLOBAL;
-                    if (lane < LK_G && cur.valid) sh.meta[d][lane] = cur.mt;
+                    if (lane < LK_G && cur.valid) {
+                        sh.meta[d][lane] = cur.mt;
+                        sh.word[d][lane] = lk_word(cur.mt.cnt, cur.mt.mode, cur.mt.lo);
+                    }
                     if (copy_iv) bytes += (uint32_t)cur.mt.cnt * (uint32_t)sizeof(IvRec);
                     if (DEN_ST && lane == 0) bytes += (uint32_t)lk_den_block(nmat);
                     // expect before issuing so the phase cannot complete early
@@ -310,42 +320,46 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                         for (int j = 0; j < LK_G; ++j) {
                             const int k = t * LK_G + j;
                             if (k >= ncomp) break;
-                            const LkMeta& mt = sh.meta[d][j];
                             const double2 dd = DEN_ST ? *reinterpret_cast<const double2*>(dens + 2 * j)
                                                       : *reinterpret_cast<const double2*>(&L.ddT[(int64_t)k * nmat + m]);
                             const double den = dd.x, dn = dd.y;
-                            const int4 mi = *reinterpret_cast<const int4*>(&mt);   // lo, cnt, last, mode
+                            const uint32_t wd = sh.word[d][j];
+                            const int32_t cnt_ = (int32_t)(wd & 31u), mode = (int32_t)((wd >> 5) & 3u);
                             const IvRec* W = sh.iv[d][j];
-                            // issued together with the meta read (always in-bounds shared memory)
+                            // issued with the meta word (always in-bounds shared memory)
                             const double a1 = W[1].E0, a2 = W[2].E0;
                             double tt, cc, ff;
-                            if (__builtin_expect(mi.w == LK_STAGED, 1)) {
+                            if (__builtin_expect(mode == LK_STAGED, 1)) {
                                 int32_t li;
-                                if (mi.y <= 4) {
-                                    // <= 3 intervals: li = #{j in 1..cnt-2 : E0_j <= E} (grids ascend)
-                                    li = (int32_t)(mi.y >= 3 && pos_le(a1, E)) + (int32_t)(mi.y >= 4 && pos_le(a2, E));
+                                if (cnt_ <= 4) {
+                                    // <= 3 intervals: li = #{j in 1..cnt-2 : E0_j <= E} (grids ascend;
+                                    // entries past the window are stale, hence the clamp to cnt-2)
+                                    li = min((int32_t)(a1 <= E) + (int32_t)(a2 <= E), cnt_ - 2);
                                 } else {
-                                    const int32_t lim = mi.z - mi.x;
-                                    li = __ldg(L.hash + mt.hrow + bin) - mi.x;
+                                    const LkMeta& mt = sh.meta[d][j];
+                                    const int32_t lim = mt.last - mt.lo;
+                                    li = __ldg(L.hash + mt.hrow + bin) - mt.lo;
                                     while (li + 1 < lim && W[li + 1].E0 <= E) ++li;
                                 }
-                                const IvRec& a = W[li];
-                                const double e0v = a.E0, e1 = W[li + 1].E0;
-                                const bool lo_clamp = mi.x + li == 0 && pos_le(E, e0v), hi_clamp = pos_le(e1, E);
+                                const double2 er = *reinterpret_cast<const double2*>(&W[li].E0);   // (E0, r)
+                                const double e0v = er.x, e1 = W[li + 1].E0;
+                                const bool lo_clamp = (wd & 128u) && li == 0 && E <= e0v, hi_clamp = e1 <= E;
                                 if (__builtin_expect(lo_clamp || hi_clamp, 0)) {
-                                    const IvRec& b = hi_clamp && !lo_clamp ? W[li + 1] : a;
+                                    const IvRec& b = hi_clamp && !lo_clamp ? W[li + 1] : W[li];
                                     tt = b.t0; cc = b.c0; ff = b.f0;
                                 } else {
-                                    const double fr = div_by_rcp_safe(__dsub_rn(E, e0v), a.d, a.r);
+                                    const IvRec& a = W[li];
+                                    const double fr = div_by_rcp_safe(__dsub_rn(E, e0v), __dsub_rn(e1, e0v), er.y);
                                     tt = __dadd_rn(a.t0, __dmul_rn(fr, a.dt));
                                     cc = __dadd_rn(a.c0, __dmul_rn(fr, a.dc));
                                     ff = __dadd_rn(a.f0, __dmul_rn(fr, a.df));
                                 }
-                            } else if (mi.w == LK_POINT) {
+                            } else if (mode == LK_POINT) {
                                 const IvRec& a = sh.iv[d][j][0];
                                 tt = a.t0; cc = a.c0; ff = a.f0;
                             } else {
-                                lk_micro_global(L, mt.g0, mi.z, mt.hrow, bin, E, tt, cc, ff);
+                                const LkMeta& mt = sh.meta[d][j];
+                                lk_micro_global(L, mt.g0, mt.last, mt.hrow, bin, E, tt, cc, ff);
                             }
                             st = __dadd_rn(st, __dmul_rn(den, tt));
                             sc = __dadd_rn(sc, __dmul_rn(den, cc));
