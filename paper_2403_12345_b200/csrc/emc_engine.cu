@@ -714,11 +714,13 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
                     c->launches += 1;
                     EMC_TRY_CUDA(cudaEventRecord(c->evt[4 * k + 1], st));
                     k_advance<<<gl, BLK, 0, st>>>(cur, (int32_t)nL, bp, c->L, c->G, c->S, lg, c->bins.p, c->qc.p,
-                                                  c->qx.p, c->ctl.p, c->cnt.p, c->M, &c->ctl.p->nLcur);
+                                                  c->qx.p, c->ctl.p, c->cnt.p, c->M, &c->ctl.p->nLcur, nxt);
                     EMC_CHECK_LAUNCH(c);
-                    k_crossing<<<gl, BLK, 0, st>>>(c->qx.p, &c->ctl.p->nX, bp, c->L, c->G, c->src, c->S, nxt,
-                                                   c->ctl.p, c->cnt.p);
-                    EMC_CHECK_LAUNCH(c);
+                    if (c->G.vacuum) {
+                        k_crossing<<<gl, BLK, 0, st>>>(c->qx.p, &c->ctl.p->nX, bp, c->L, c->G, c->src, c->S, nxt,
+                                                       c->ctl.p, c->cnt.p);
+                        EMC_CHECK_LAUNCH(c);
+                    }
                     EMC_TRY_CUDA(cudaEventRecord(c->evt[4 * k + 2], st));
                     k_collision<<<gl, BLK, 0, st>>>(c->qc.p, &c->ctl.p->nC, bp, c->L, c->G, c->src, c->S, lg, sv,
                                                     c->bins.p, nxt, c->ctl.p, c->cnt.p);
@@ -788,11 +790,13 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             EMC_CHECK_LAUNCH(c);
             EMC_TRY_CUDA(cudaEventRecord(c->ev[2], st));
             k_advance<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(q, (int32_t)nL, bp, c->L, c->G, c->S, lg, c->bins.p,
-                                                              c->qc.p, c->qx.p, c->ctl.p, c->cnt.p, c->M, nullptr);
+                                                              c->qc.p, c->qx.p, c->ctl.p, c->cnt.p, c->M, nullptr, nxt);
             EMC_CHECK_LAUNCH(c);
-            k_crossing<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(c->qx.p, &c->ctl.p->nX, bp, c->L, c->G, c->src, c->S,
-                                                               nxt, c->ctl.p, c->cnt.p);
-            EMC_CHECK_LAUNCH(c);
+            if (c->G.vacuum) {       // leakage: end and refill (reflective problems cross inside k_advance)
+                k_crossing<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(c->qx.p, &c->ctl.p->nX, bp, c->L, c->G, c->src,
+                                                                   c->S, nxt, c->ctl.p, c->cnt.p);
+                EMC_CHECK_LAUNCH(c);
+            }
             EMC_TRY_CUDA(cudaEventRecord(c->ev[3], st));
             k_collision<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(c->qc.p, &c->ctl.p->nC, bp, c->L, c->G, c->src,
                                                                 c->S, lg, sv, c->bins.p, nxt, c->ctl.p, c->cnt.p);

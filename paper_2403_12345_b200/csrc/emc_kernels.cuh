@@ -312,18 +312,44 @@ __device__ __forceinline__ void score_bins(double* bins, bool valid, int32_t bas
     }
 }
 
-// K:713-811 (first half): sample the flight distance, score the segment,
-// move.  Collisions go to q_col, surface hits to q_cross.
+// K:782-811: cross surface d.surf -- reflect on an outer box plane, nudge
+// past the surface, update cell and material (in registers)
+__device__ __forceinline__ void cross_surface(P0& a, P1& b, P3& d, const DGeom& G)
+{
+    const int32_t surf = d.surf;
+    if (surf >= SURF_XMIN && surf <= SURF_ZMAX) {
+        if (surf == SURF_XMIN || surf == SURF_XMAX) b.dx = -b.dx;
+        else if (surf == SURF_YMIN || surf == SURF_YMAX) b.dy = -b.dy;
+        else b.dz = -b.dz;
+    }
+    a.x = __dadd_rn(a.x, __dmul_rn(b.dx, kNudge));
+    a.y = __dadd_rn(a.y, __dmul_rn(b.dy, kNudge));
+    a.z = __dadd_rn(a.z, __dmul_rn(b.dz, kNudge));
+    if (surf == SURF_CYL) {
+        if (d.kind == KIND_FUEL) { d.kind = KIND_MOD; d.axial = -1; }
+        else { d.kind = KIND_FUEL; d.axial = axial_index(a.z, G.n_axial, G.height); }
+    } else if (surf >= SURF_AXIAL_BASE && surf < SURF_LATTICE) {
+        int32_t jpl = surf - SURF_AXIAL_BASE;
+        d.axial = b.dz > 0.0 ? jpl : jpl - 1;
+    }
+    d.mat = d.kind == KIND_FUEL ? G.fuel_mats[d.axial] : G.mod_mat;
+}
+
+// K:713-811: sample the flight distance, score the segment, move.
+// Collisions go to q_col; surface crossings are completed here (the second
+// half of the reference's advance) and go straight back to the lookup queue
+// q_next -- except vacuum leakage, which k_crossing ends and refills.
 __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __restrict__ q, int32_t n, BatchP bp,
                                                  DLib L, DGeom G, DSlots S, DLog lg, double* bins,
                                                  int32_t* q_col, int32_t* q_cross, Ctl* ctl,
-                                                 unsigned long long* cnt, DMesh M, const unsigned int* nptr)
+                                                 unsigned long long* cnt, DMesh M, const unsigned int* nptr,
+                                                 int32_t* q_next)
 {
     if (nptr) n = (int32_t)*nptr;        // tail mode: queue length lives on the device
     unsigned long long interp_score = 0;
     EMC_WARP_LOOP(n) {
         int64_t i = emc_base_ + lane_id();
-        bool valid = i < n, to_col = false, to_cross = false;
+        bool valid = i < n, to_col = false, to_cross = false, leak = false;
         int32_t s = valid ? q[i] : 0;
         double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         int32_t base = 0;
@@ -381,6 +407,8 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
                     } else {
                         to_col = !crossing;
                         to_cross = crossing;
+                        leak = crossing && G.vacuum && surf >= SURF_XMIN && surf <= SURF_ZMAX;
+                        if (crossing && !leak) cross_surface(a, b, d, G);
                     }
                     p.a = a; p.b = b;
                 }
@@ -415,7 +443,8 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
         }
         if (to_col || to_cross) S.ps[s].d = d;
         queue_push(q_col, &ctl->nC, s, to_col);
-        queue_push(q_cross, &ctl->nX, s, to_cross);
+        queue_push(q_next, &ctl->nL2, s, to_cross && !leak);
+        if (G.vacuum) queue_push(q_cross, &ctl->nX, s, to_cross && leak);
     }
     warp_add_u64(cnt + CNT_INTERP_SCORE, interp_score);
 }
@@ -446,23 +475,8 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_crossing(const int32_t* _
                 leaks += 1;
                 maxdraws = max(maxdraws, (unsigned long long)d.draws);
                 maxhist = max(maxhist, (unsigned long long)d.histlog);
-            } else {
-                if (surf >= SURF_XMIN && surf <= SURF_ZMAX) {
-                    if (surf == SURF_XMIN || surf == SURF_XMAX) b.dx = -b.dx;
-                    else if (surf == SURF_YMIN || surf == SURF_YMAX) b.dy = -b.dy;
-                    else b.dz = -b.dz;
-                }
-                a.x = __dadd_rn(a.x, __dmul_rn(b.dx, kNudge));
-                a.y = __dadd_rn(a.y, __dmul_rn(b.dy, kNudge));
-                a.z = __dadd_rn(a.z, __dmul_rn(b.dz, kNudge));
-                if (surf == SURF_CYL) {
-                    if (d.kind == KIND_FUEL) { d.kind = KIND_MOD; d.axial = -1; }
-                    else { d.kind = KIND_FUEL; d.axial = axial_index(a.z, G.n_axial, G.height); }
-                } else if (surf >= SURF_AXIAL_BASE && surf < SURF_LATTICE) {
-                    int32_t jpl = surf - SURF_AXIAL_BASE;
-                    d.axial = b.dz > 0.0 ? jpl : jpl - 1;
-                }
-                d.mat = d.kind == KIND_FUEL ? G.fuel_mats[d.axial] : G.mod_mat;
+            } else {                     // (k_advance completes non-leaking crossings itself)
+                cross_surface(a, b, d, G);
                 p.a = a; p.b = b; p.d = d;
             }
         }
