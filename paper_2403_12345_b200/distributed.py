@@ -37,9 +37,11 @@ class World:
     size: int = 1
     device_backend: bool = False        # True: NCCL (tensors must be on CUDA)
 
+    forced: bool = False                # EMC_FORCE_COLLECTIVES=1: collectives even at size 1
+
     @property
     def distributed(self) -> bool:
-        return self.size > 1
+        return self.size > 1 or self.forced
 
 
 def current_world() -> World:
@@ -49,7 +51,9 @@ def current_world() -> World:
         return World()
     if not (dist.is_available() and dist.is_initialized()):
         return World()
-    return World(dist.get_rank(), dist.get_world_size(), dist.get_backend() == "nccl")
+    import os
+    return World(dist.get_rank(), dist.get_world_size(), dist.get_backend() == "nccl",
+                 os.environ.get("EMC_FORCE_COLLECTIVES") == "1")
 
 
 def block_of(rank: int, size: int, ppb: int) -> tuple[int, int]:

@@ -63,3 +63,39 @@ def test_multirank_matches_reference_fingerprint(golden, world):
         assert fp == run["fingerprint"], (rank, fp)
         assert np.array_equal(np.array(keff), z["keff"])
         assert nbank == run["bank_len"]
+
+
+def _nccl_rank(q, run, pm, port):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), EMC_FORCE_COLLECTIVES="1")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        import paper_2403_12345_b200 as P
+        from paper_2403_12345_b200.distributed import current_world
+        w = current_world()
+        assert w.device_backend and w.distributed
+        cell = P.Pincell(n_axial=pm["n_axial"], fuel_material_ids=pm["fuel_material_ids"],
+                         moderator_material_id=pm["moderator_material_id"])
+        res = P.run_replicated(P.RunConfig(**run["config"]), golden_library(run["problem"]), cell)
+        q.put((res.physics_fingerprint(), len(res.bank)))
+    except Exception as e:  # noqa: BLE001
+        q.put((f"error: {e!r}", None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_collective_path_single_gpu(golden):
+    """The multi-GPU code path proper -- NCCL on device tensors, zero-copy
+    views of libemc's bank, the windowed all-to-all exchange, the device
+    source window and the final bank all-gather -- forced on at world size 1
+    (the only NCCL world one GPU allows): the reference's C1 fingerprint."""
+    run = golden["runs"]["c1_event"]
+    pm = golden["problems"]["c1"]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_rank, args=(q, run, pm, _free_port()))
+    p.start()
+    fp, nbank = q.get(timeout=600)
+    p.join(60)
+    assert fp == run["fingerprint"], fp
+    assert nbank == run["bank_len"]
