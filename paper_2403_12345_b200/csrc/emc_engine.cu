@@ -760,7 +760,7 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
                 if (rc) return rc;
                 q = c->qs.p;
                 host_cnt[CNT_SORTS] += 1;
-                if (c->reorder) {
+                if (c->reorder && !c->staged) {
                     PState* dst = c->ps_cur == c->ps.p ? c->ps2.p : c->ps.p;
                     k_reorder<<<grid_for(nL, BLK, 1 << 30), BLK, 0, st>>>(c->qs.p, (int32_t)nL, c->ps_cur, dst);
                     EMC_CHECK_LAUNCH(c);
@@ -772,8 +772,16 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             look_inv++;
             EMC_TRY_CUDA(cudaEventRecord(c->ev[1], st));
             if (c->staged) {
+                // the staged lookup moves the lines into sorted order itself (fused reorder)
+                PState* rdst = nullptr;
+                if (do_sort && c->reorder) rdst = c->ps_cur == c->ps.p ? c->ps2.p : c->ps.p;
                 EMC_TRY_CUDA(lk_launch<0>(c->lk_cfg, c->L, q, nL, c->S, cf.fused, c->cnt.p, nullptr, nullptr, nullptr,
-                                          c->sm_count, c->lk_smem, st));
+                                          c->sm_count, c->lk_smem, st, nullptr, rdst));
+                if (rdst) {
+                    c->ps_cur = rdst;
+                    c->S.ps = rdst;
+                    q = c->iota.p;
+                }
             } else switch (c->lookup_block) {
             case 1024:
                 k_lookup<1024><<<grid_for(nL, 1024, c->sm_count), 1024, 0, st>>>(q, (int32_t)nL, c->L, c->S,

@@ -214,7 +214,7 @@ template <int MODE, bool DEN_ST, int NW, int MINB>
 __global__ void __launch_bounds__(NW * 32, MINB)
     k_lookup_staged(const int32_t* __restrict__ q, int32_t n, DLib L, DSlots S, int32_t fused,
                     unsigned long long* cnt, const double* __restrict__ bE, const int32_t* __restrict__ bM,
-                    double* __restrict__ bout, const unsigned int* nptr)
+                    double* __restrict__ bout, const unsigned int* nptr, PState* __restrict__ rdst)
 {
     if (nptr) n = (int32_t)*nptr;        // tail mode: queue length lives on the device
     extern __shared__ __align__(128) unsigned char lk_raw[];
@@ -243,7 +243,15 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         int32_t s = 0, m = 0, grp = 0, bin = 0;
         double E = 1.0;
         if (pend) {
-            if (MODE == 0) {
+            if (MODE == 0 && rdst) {
+                // fused reorder (replaces k_reorder): move the particle's line to
+                // queue position i, which becomes its slot from here on
+                const PState line = S.ps[q[i]];
+                rdst[i] = line;
+                s = (int32_t)i;
+                E = line.a.E;
+                m = line.d.mat;
+            } else if (MODE == 0) {
                 s = q[i];
                 E = S.ps[s].a.E;
                 m = S.ps[s].d.mat;
@@ -380,7 +388,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
             if (mine) {
                 if (MODE == 0) {
                     P2 c; c.t = st; c.c = sc; c.f = sf; c.nsf = snf;
-                    S.ps[s].c = c;
+                    (rdst ? rdst : S.ps)[s].c = c;
                 } else {
                     bout[i] = st + sc + sf + snf;
                 }
@@ -409,29 +417,31 @@ constexpr int lk_cfg_minb(int c) { return c == 0 ? 1 : 2; }
 template <int MODE, int CFG>
 inline cudaError_t lk_launch_cfg(const DLib& L, const int32_t* q, int64_t n, DSlots S, int32_t fused,
                                  unsigned long long* cnt, const double* bE, const int32_t* bM, double* bout,
-                                 int sm_count, size_t smem, cudaStream_t st, const unsigned int* nptr)
+                                 int sm_count, size_t smem, cudaStream_t st, const unsigned int* nptr,
+                                 PState* rdst)
 {
     constexpr int NW = lk_cfg_warps(CFG), MB = lk_cfg_minb(CFG);
     constexpr int64_t chunk = (NW - 1) * 32;
     const unsigned nb = (unsigned)std::min<int64_t>((n + chunk - 1) / chunk, (int64_t)sm_count * MB);
     if (L.den_staged)
         k_lookup_staged<MODE, true, NW, MB><<<nb, NW * 32, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM, bout,
-                                                                       nptr);
+                                                                       nptr, rdst);
     else
         k_lookup_staged<MODE, false, NW, MB><<<nb, NW * 32, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM,
-                                                                        bout, nptr);
+                                                                        bout, nptr, rdst);
     return cudaGetLastError();
 }
 
 template <int MODE>
 inline cudaError_t lk_launch(int cfg, const DLib& L, const int32_t* q, int64_t n, DSlots S, int32_t fused,
                              unsigned long long* cnt, const double* bE, const int32_t* bM, double* bout, int sm_count,
-                             size_t smem, cudaStream_t st, const unsigned int* nptr = nullptr)
+                             size_t smem, cudaStream_t st, const unsigned int* nptr = nullptr,
+                             PState* rdst = nullptr)
 {
     switch (cfg) {
-    case 1: return lk_launch_cfg<MODE, 1>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, nptr);
-    case 2: return lk_launch_cfg<MODE, 2>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, nptr);
-    default: return lk_launch_cfg<MODE, 0>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, nptr);
+    case 1: return lk_launch_cfg<MODE, 1>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, nptr, rdst);
+    case 2: return lk_launch_cfg<MODE, 2>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, nptr, rdst);
+    default: return lk_launch_cfg<MODE, 0>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, nptr, rdst);
     }
 }
 
