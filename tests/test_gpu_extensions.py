@@ -108,3 +108,54 @@ def test_pwr_assembly_c2_scale_staged_equals_plain():
         finally:
             os.environ.pop("EMC_LOOKUP", None)
     assert out["staged"] == out["plain"]
+
+
+def _edge_library():
+    """A 20-nuclide fuel group that drives every path of the staged lookup:
+    a 1-point nuclide (point window), a 2-point nuclide, a nuclide whose grid
+    leaves the guard-free division range (IEEE-division fallback for the whole
+    nuclide), exact duplicate energies across nuclides, and long/short grids
+    (staged windows and over-wide windows that fall back to the global path)."""
+    rng = np.random.default_rng(5)
+    nucs = []
+
+    def nuc(grid, fiss):
+        g = np.asarray(grid, np.float64)
+        n = g.shape[0]
+        s = rng.uniform(2.0, 8.0, n)
+        c = rng.uniform(0.3, 2.5, n)
+        f = rng.uniform(1.5, 8.0, n) if fiss else np.full(n, 1e-7)
+        return P.NuclideXS(g, s + c + f, s, c, f, 2.43 if fiss else 0.0)
+
+    nucs.append(nuc([1.0e-5], True))                                  # glen 1
+    nucs.append(nuc([1.0e-5, 2.0e7], False))                          # glen 2
+    nucs.append(nuc([1.0e-70, 1.0e-69, 1.0, 2.0e7], False))           # outside the safe range
+    shared = np.exp(np.linspace(np.log(1e-5), np.log(2e7), 400))
+    for k in range(17):
+        if k % 5 == 0:
+            g = shared.copy()                                          # identical grids
+        else:
+            npts = int(rng.integers(20, 3000))
+            g = np.sort(np.exp(rng.uniform(np.log(1e-5), np.log(2e7), npts)))
+            g[0], g[-1] = 1e-5, 2e7
+            g = np.unique(g)
+        nucs.append(nuc(g, k % 3 == 0))
+    mod = [nuc(np.exp(np.linspace(np.log(1e-5), np.log(2e7), 100)), False) for _ in range(3)]
+    nucs += mod
+    dens = rng.uniform(6e-4, 6e-3, 20)
+    mats = [P.Material(m, [(i, float(dens[i] * (1 + 0.1 * m))) for i in range(20)]) for m in range(2)]
+    mats.append(P.Material(2, [(20 + i, 0.05) for i in range(3)]))
+    lib = P.Library(nucs, mats)
+    cell = P.Pincell(n_axial=2, fuel_material_ids=[0, 1], moderator_material_id=2)
+    return lib, cell
+
+
+@pytest.mark.parametrize("cap", [3000, 256])
+def test_edge_library_staged_paths_match_oracle(cap):
+    lib, cell = _edge_library()
+    cfg = P.RunConfig(particles_per_batch=3000, inactive_batches=2, active_batches=2, mode="event",
+                      reduction="deterministic", max_in_flight=cap)
+    res = P.run_replicated(cfg, lib, cell)
+    ores = driver.run(dict(cfg.__dict__), lib.arrays(), cell.as_tuple())
+    assert res.physics_fingerprint() == driver.fingerprint(ores)
+    assert res.counters["interp_transport"] == ores["counters"]["interp_transport"]
