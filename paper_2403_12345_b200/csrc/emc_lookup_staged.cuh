@@ -43,11 +43,14 @@ struct __align__(16) LkMeta {
     int32_t g0, hrow;              // global fallback
 };
 
-// fast-path meta word: window size (bits 0-4), mode (5-6), window starts at
-// the nuclide's first point (7)
-__host__ __device__ constexpr uint32_t lk_word(int32_t cnt, int32_t mode, int32_t lo)
+// Per-(chunk, nuclide) meta word: window size (bits 0-4), mode (5-6),
+// "edge" (7) = the window touches the nuclide's first or last grid point, the
+// only case in which the reference's end clamps (K:600-612) can apply.  The
+// consumers' fast path is exactly `word <= 4`: a staged window of <= 3
+// intervals away from both grid ends -- no clamp tests, no scan.
+__host__ __device__ constexpr uint32_t lk_word(int32_t cnt, int32_t mode, int32_t lo, int32_t last)
 {
-    return (uint32_t)(cnt & 31) | ((uint32_t)mode << 5) | ((uint32_t)(lo == 0) << 7);
+    return (uint32_t)(cnt & 31) | ((uint32_t)mode << 5) | ((uint32_t)(lo == 0 || lo + cnt - 1 >= last) << 7);
 }
 
 struct __align__(128) LkShared {
@@ -180,6 +183,43 @@ __device__ __forceinline__ bool pos_le(double a, double b)
     return __double_as_longlong(a) <= __double_as_longlong(b);
 }
 
+// Every case the fast path does not take: a staged window near a grid end
+// (clamps, K:600-612) or wider than 3 intervals (scan from the hash bound),
+// a 1-point nuclide, or a (chunk, nuclide) served from global memory.
+__device__ __forceinline__ void lk_micro_slow(const DLib& L, const LkMeta& mt, uint32_t wd, const IvRec* W, double a1,
+                                           double a2, int32_t bin, double E, double& tt, double& cc, double& ff)
+{
+    const int32_t cnt_ = (int32_t)(wd & 31u), mode = (int32_t)((wd >> 5) & 3u);
+    if (mode == LK_POINT) {
+        tt = W[0].t0; cc = W[0].c0; ff = W[0].f0;
+        return;
+    }
+    if (mode == LK_GLOBAL) {
+        lk_micro_global(L, mt.g0, mt.last, mt.hrow, bin, E, tt, cc, ff);
+        return;
+    }
+    int32_t li;
+    if (cnt_ <= 4) {
+        li = min((int32_t)(a1 <= E) + (int32_t)(a2 <= E), cnt_ - 2);
+    } else {
+        const int32_t lim = mt.last - mt.lo;
+        li = __ldg(L.hash + mt.hrow + bin) - mt.lo;
+        while (li + 1 < lim && W[li + 1].E0 <= E) ++li;
+    }
+    const double e0v = W[li].E0, e1 = W[li + 1].E0;
+    const bool lo_clamp = mt.lo + li == 0 && E <= e0v, hi_clamp = e1 <= E;
+    if (lo_clamp || hi_clamp) {
+        const IvRec& b = hi_clamp && !lo_clamp ? W[li + 1] : W[li];
+        tt = b.t0; cc = b.c0; ff = b.f0;
+    } else {
+        const IvRec& a = W[li];
+        const double fr = div_by_rcp_safe(__dsub_rn(E, e0v), __dsub_rn(e1, e0v), a.r);
+        tt = __dadd_rn(a.t0, __dmul_rn(fr, a.dt));
+        cc = __dadd_rn(a.c0, __dmul_rn(fr, a.dc));
+        ff = __dadd_rn(a.f0, __dmul_rn(fr, a.df));
+    }
+}
+
 // One producer lane's view of nuclide k of the current pass.
 struct LkNext {
     LkMeta mt;
@@ -305,7 +345,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                     const bool copy_iv = lane < LK_G && cur.valid && cur.mt.mode != LK_GLOBAL;
                     if (lane < LK_G && cur.valid) {
                         sh.meta[d][lane] = cur.mt;
-                        sh.word[d][lane] = lk_word(cur.mt.cnt, cur.mt.mode, cur.mt.lo);
+                        sh.word[d][lane] = lk_word(cur.mt.cnt, cur.mt.mode, cur.mt.lo, cur.mt.last);
                     }
                     if (copy_iv) bytes += (uint32_t)cur.mt.cnt * (uint32_t)sizeof(IvRec);
                     if (DEN_ST && lane == 0) bytes += (uint32_t)lk_den_block(nmat);
@@ -332,42 +372,25 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                                                       : *reinterpret_cast<const double2*>(&L.ddT[(int64_t)k * nmat + m]);
                             const double den = dd.x, dn = dd.y;
                             const uint32_t wd = sh.word[d][j];
-                            const int32_t cnt_ = (int32_t)(wd & 31u), mode = (int32_t)((wd >> 5) & 3u);
                             const IvRec* W = sh.iv[d][j];
                             // issued with the meta word (always in-bounds shared memory)
                             const double a1 = W[1].E0, a2 = W[2].E0;
                             double tt, cc, ff;
-                            if (__builtin_expect(mode == LK_STAGED, 1)) {
-                                int32_t li;
-                                if (cnt_ <= 4) {
-                                    // <= 3 intervals: li = #{j in 1..cnt-2 : E0_j <= E} (grids ascend;
-                                    // entries past the window are stale, hence the clamp to cnt-2)
-                                    li = min((int32_t)(a1 <= E) + (int32_t)(a2 <= E), cnt_ - 2);
-                                } else {
-                                    const LkMeta& mt = sh.meta[d][j];
-                                    const int32_t lim = mt.last - mt.lo;
-                                    li = __ldg(L.hash + mt.hrow + bin) - mt.lo;
-                                    while (li + 1 < lim && W[li + 1].E0 <= E) ++li;
-                                }
+                            if (__builtin_expect(wd <= 4u, 1)) {
+                                // <= 3 interior intervals: li = #{j in 1..cnt-2 : E0_j <= E}
+                                // (grids ascend; entries past the window are stale, hence
+                                // the clamp to cnt-2).  Away from the grid ends E lies in
+                                // [E0, E1) of interval li: no clamp can apply.
+                                const int32_t li = min((int32_t)(a1 <= E) + (int32_t)(a2 <= E), (int32_t)wd - 2);
                                 const double2 er = *reinterpret_cast<const double2*>(&W[li].E0);   // (E0, r)
-                                const double e0v = er.x, e1 = W[li + 1].E0;
-                                const bool lo_clamp = (wd & 128u) && li == 0 && E <= e0v, hi_clamp = e1 <= E;
-                                if (__builtin_expect(lo_clamp || hi_clamp, 0)) {
-                                    const IvRec& b = hi_clamp && !lo_clamp ? W[li + 1] : W[li];
-                                    tt = b.t0; cc = b.c0; ff = b.f0;
-                                } else {
-                                    const IvRec& a = W[li];
-                                    const double fr = div_by_rcp_safe(__dsub_rn(E, e0v), __dsub_rn(e1, e0v), er.y);
-                                    tt = __dadd_rn(a.t0, __dmul_rn(fr, a.dt));
-                                    cc = __dadd_rn(a.c0, __dmul_rn(fr, a.dc));
-                                    ff = __dadd_rn(a.f0, __dmul_rn(fr, a.df));
-                                }
-                            } else if (mode == LK_POINT) {
-                                const IvRec& a = sh.iv[d][j][0];
-                                tt = a.t0; cc = a.c0; ff = a.f0;
+                                const double e1 = W[li + 1].E0;
+                                const IvRec& a = W[li];
+                                const double fr = div_by_rcp_safe(__dsub_rn(E, er.x), __dsub_rn(e1, er.x), er.y);
+                                tt = __dadd_rn(a.t0, __dmul_rn(fr, a.dt));
+                                cc = __dadd_rn(a.c0, __dmul_rn(fr, a.dc));
+                                ff = __dadd_rn(a.f0, __dmul_rn(fr, a.df));
                             } else {
-                                const LkMeta& mt = sh.meta[d][j];
-                                lk_micro_global(L, mt.g0, mt.last, mt.hrow, bin, E, tt, cc, ff);
+                                lk_micro_slow(L, sh.meta[d][j], wd, W, a1, a2, bin, E, tt, cc, ff);
                             }
                             st = __dadd_rn(st, __dmul_rn(den, tt));
                             sc = __dadd_rn(sc, __dmul_rn(den, cc));
