@@ -322,14 +322,15 @@ __global__ void __launch_bounds__(NW * 32, MINB)
             const int32_t bmin = sh.bmin, bmax = sh.bmax;
             const int32_t e0 = __ldg(L.grp_off + G), ncomp = __ldg(L.grp_off + G + 1) - e0;
             double st = 0.0, sc = 0.0, sf = 0.0, snf = 0.0;
-            double* ck = nullptr;
-            int64_t cks = 1;
-            if (MODE == 0) { if (fused) { ck = S.ckpt + s; cks = S.nslots; } }
-            else { ck = bout + n + i; cks = n; }
+            // sigma_t checkpoints: row r of this particle at ckb[r * cks] (formed
+            // at the store, not kept live through the nuclide loop)
+            const bool ckon = MODE == 1 || fused;
+            const int64_t cks = MODE == 0 ? S.nslots : (int64_t)n;
             const int nst = (ncomp + LK_G - 1) / LK_G;
 
             if (ncomp < LK_MIN_NUC) {
-                if (mine) macro_tcf(L, m, E, st, sc, sf, snf, ck, nck, cks);
+                if (mine) macro_tcf(L, m, E, st, sc, sf, snf,
+                                    ckon ? (MODE == 0 ? S.ckpt + s : bout + n + i) : nullptr, nck, cks);
             } else if (producer) {
                 // lane j < LK_G owns nuclide 8t+j of every stage; its global
                 // reads for stage t+1 are issued before it waits for slot t
@@ -399,9 +400,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                         }
                         // prefix checkpoint after every kCkptStride (= 2 stages) nuclides
                         static_assert(kCkptStride == 2 * LK_G, "checkpoint every second stage");
-                        if (ck && (t & 1) && (t + 1) * LK_G <= ncomp) {
+                        if (ckon && (t & 1) && (t + 1) * LK_G <= ncomp) {
                             const int32_t row = t >> 1;
-                            if (row < nck) ck[(int64_t)row * cks] = st;
+                            double* ckb = MODE == 0 ? S.ckpt + s : bout + n + i;
+                            if (row < nck) ckb[(int64_t)row * cks] = st;
                         }
                     }
                     __syncwarp();
