@@ -526,29 +526,51 @@ __device__ __forceinline__ int32_t select_nuclide(const DLib& L, const double* c
     }
     int32_t ksel = e1 - 1;
     pt_sel = 0.0;
-    // walk in groups of SN nuclides: the composition, hash and record reads
-    // of a group are independent and issued together; the comparison walk
-    // over the group stays sequential (same cum and pt values as K:846-852)
+    // walk in groups of SN nuclides, software-pipelined one group ahead: the
+    // composition entries and hash bounds of group g+1 are loaded while the
+    // records of group g are in flight, so each group costs one dependent
+    // gather instead of three; the comparison walk stays sequential (same cum
+    // and pt values as K:846-852)
 #ifndef EMC_WALK_SN
-#define EMC_WALK_SN 2
+#define EMC_WALK_SN 1
 #endif
     constexpr int SN = EMC_WALK_SN;
-    for (int32_t k0 = e0 + c * kCkptStride; k0 < e1; k0 += SN) {
+    const int32_t kstart = e0 + c * kCkptStride;
+    double nden[SN];
+    int32_t ng0[SN], nlast[SN], nh[SN];
+    #pragma unroll
+    for (int u = 0; u < SN; ++u) {
+        const Comp cc = L.comp[min(kstart + u, e1 - 1)];
+        nden[u] = cc.den; ng0[u] = cc.g0; nlast[u] = cc.glen - 1;
+        nh[u] = nlast[u] > 0 ? __ldg(L.hash + (int64_t)cc.nid * L.nbins + bin) : 0;
+    }
+    for (int32_t k0 = kstart; k0 < e1; k0 += SN) {
         double den[SN], e0v[SN], t0[SN], e1v[SN], t1[SN];
-        int32_t st[SN];
+        int32_t st[SN], g0[SN], lastv[SN], hv[SN];
+        #pragma unroll
+        for (int u = 0; u < SN; ++u) { den[u] = nden[u]; g0[u] = ng0[u]; lastv[u] = nlast[u]; hv[u] = nh[u]; }
+        #pragma unroll
+        for (int u = 0; u < SN; ++u) {            // records of this group
+            const Rec* __restrict__ R = L.rec + g0[u];
+            const double2 p0 = *reinterpret_cast<const double2*>(&R[hv[u]].E);        // (E, t) of point i
+            const double2 p1 = *reinterpret_cast<const double2*>(&R[min(hv[u] + 1, lastv[u])].E);
+            e0v[u] = p0.x; t0[u] = p0.y; e1v[u] = p1.x; t1[u] = p1.y;
+        }
+        if (k0 + SN < e1) {                       // next group's entries and hash bounds
+            #pragma unroll
+            for (int u = 0; u < SN; ++u) {
+                const Comp cc = L.comp[min(k0 + SN + u, e1 - 1)];
+                nden[u] = cc.den; ng0[u] = cc.g0; nlast[u] = cc.glen - 1;
+                nh[u] = nlast[u] > 0 ? __ldg(L.hash + (int64_t)cc.nid * L.nbins + bin) : 0;
+            }
+        }
         #pragma unroll
         for (int u = 0; u < SN; ++u) {
-            const int32_t k = min(k0 + u, e1 - 1);
-            const Comp cc = L.comp[k];
-            den[u] = cc.den;
-            const Rec* __restrict__ R = L.rec + cc.g0;
-            const int32_t last = cc.glen - 1;
-            int32_t i = last > 0 ? __ldg(L.hash + (int64_t)cc.nid * L.nbins + bin) : 0;
-            const double2 p0 = *reinterpret_cast<const double2*>(&R[i].E);        // (E, t) of point i
-            const double2 p1 = *reinterpret_cast<const double2*>(&R[min(i + 1, last)].E);
-            e0v[u] = p0.x; t0[u] = p0.y; e1v[u] = p1.x; t1[u] = p1.y;
+            const int32_t last = lastv[u];
             if (last == 0) { st[u] = 1; continue; }
+            int32_t i = hv[u];
             if (e1v[u] <= E && i + 1 < last) {     // rare: bracket beyond the hashed lower bound
+                const Rec* __restrict__ R = L.rec + g0[u];
                 do {
                     ++i; e0v[u] = e1v[u]; t0[u] = t1[u];
                     const double2 q = *reinterpret_cast<const double2*>(&R[i + 1].E);
