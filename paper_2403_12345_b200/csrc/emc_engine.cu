@@ -150,7 +150,7 @@ struct emc_ctx {
 
     // queues + sort scratch
     DBuf<int32_t> qa, qb, qs, qc, qx;
-    DBuf<uint32_t> keys_in, keys_out;
+    DBuf<uint32_t> keys_in, keys_out, keys_b;   // keys_in / keys_b: push-time keys paired with qa / qb
     DBuf<unsigned char> cub_tmp;
 
     // fission bank: raw appends + canonical (sorted) copy
@@ -223,7 +223,7 @@ extern "C" void emc_destroy(emc_ctx* c)
         b->release();
     c->ps.release(); c->ps2.release(); c->iota.release(); c->rec.release(); c->comp.release();
     c->mat_group.release(); c->grp_off.release(); c->gnuc.release(); c->ddT.release(); c->denS.release(); c->iv.release(); c->nsafe.release();
-    c->keys_in.release(); c->keys_out.release(); c->cub_tmp.release();
+    c->keys_in.release(); c->keys_out.release(); c->keys_b.release(); c->cub_tmp.release();
     c->bkey_in.release(); c->bkey_out.release(); c->lkey_in.release(); c->lkey_out.release();
     c->lg_gid.release(); c->cnt.release(); c->ctl.release();
     c->sites.release(); c->banks[0].release(); c->banks[1].release();
@@ -519,7 +519,7 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
     rc |= c->ckpt.alloc(std::max<int64_t>(1, (int64_t)c->nck * nslots));
     for (auto* b : {&c->qa, &c->qb, &c->qs, &c->qc, &c->qx})
         rc |= b->alloc(nslots);
-    rc |= c->keys_in.alloc(nslots); rc |= c->keys_out.alloc(nslots);
+    rc |= c->keys_in.alloc(nslots); rc |= c->keys_out.alloc(nslots); rc |= c->keys_b.alloc(nslots);
     rc |= c->bins.alloc(c->n_bins); rc |= c->bins_init.alloc(c->n_bins); rc |= c->bins_out.alloc(c->n_bins);
     if (rc) return EMC_E_OOM;
     if (rc) return EMC_E_OOM;
@@ -692,8 +692,14 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
     } else {
         int32_t* cur = c->qa.p;
         int32_t* nxt = c->qb.p;
+        // push-time sort keys (staged lookup's energy-major key), paired with the queues
+        uint32_t* kcur = c->keys_in.p;
+        uint32_t* knxt = c->keys_b.p;
+        auto qk = [&](uint32_t* k) {
+            return QKeys{c->staged ? k : nullptr, c->ebin_bits, c->ebin_shift, c->mat_bits, c->band_bits};
+        };
         k_source_init<<<grid_for(n0, BLK, maxb), BLK, 0, st>>>(bp, c->L, c->G, c->src, c->S, (int32_t)n0, cur,
-                                                               c->ctl.p, c->cnt.p);
+                                                               c->ctl.p, c->cnt.p, qk(kcur));
         EMC_CHECK_LAUNCH(c);
         EMC_TRY_CUDA(cudaMemcpyAsync(c->ctl_host, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
         EMC_TRY_CUDA(cudaStreamSynchronize(st));
@@ -714,21 +720,22 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
                     c->launches += 1;
                     EMC_TRY_CUDA(cudaEventRecord(c->evt[4 * k + 1], st));
                     k_advance<<<gl, BLK, 0, st>>>(cur, (int32_t)nL, bp, c->L, c->G, c->S, lg, c->bins.p, c->qc.p,
-                                                  c->qx.p, c->ctl.p, c->cnt.p, c->M, &c->ctl.p->nLcur, nxt);
+                                                  c->qx.p, c->ctl.p, c->cnt.p, c->M, &c->ctl.p->nLcur, nxt, qk(knxt));
                     EMC_CHECK_LAUNCH(c);
                     if (c->G.vacuum) {
                         k_crossing<<<gl, BLK, 0, st>>>(c->qx.p, &c->ctl.p->nX, bp, c->L, c->G, c->src, c->S, nxt,
-                                                       c->ctl.p, c->cnt.p);
+                                                       c->ctl.p, c->cnt.p, qk(knxt));
                         EMC_CHECK_LAUNCH(c);
                     }
                     EMC_TRY_CUDA(cudaEventRecord(c->evt[4 * k + 2], st));
                     k_collision<<<gl, BLK, 0, st>>>(c->qc.p, &c->ctl.p->nC, bp, c->L, c->G, c->src, c->S, lg, sv,
-                                                    c->bins.p, nxt, c->ctl.p, c->cnt.p);
+                                                    c->bins.p, nxt, c->ctl.p, c->cnt.p, qk(knxt));
                     EMC_CHECK_LAUNCH(c);
                     k_tail_end<<<1, 1, 0, st>>>(c->ctl.p, c->cnt.p);
                     EMC_CHECK_LAUNCH(c);
                     EMC_TRY_CUDA(cudaEventRecord(c->evt[4 * k + 3], st));
                     std::swap(cur, nxt);
+                    std::swap(kcur, knxt);
                 }
                 EMC_TRY_CUDA(cudaMemcpyAsync(c->ctl_host, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
                 EMC_TRY_CUDA(cudaStreamSynchronize(st));
@@ -747,16 +754,13 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             bool do_sort = cf.sort_enabled && nL > 1 && (look_inv % cf.sort_every) == 0;
             EMC_TRY_CUDA(cudaEventRecord(c->ev[0], st));
             if (do_sort) {
-                if (c->staged)
-                    k_sort_keys<true><<<grid_for(nL, BLK, 1 << 30), BLK, 0, st>>>(
-                        cur, (int32_t)nL, c->ps_cur, c->L, c->keys_in.p, c->ebin_bits, c->ebin_shift, c->mat_bits,
-                        c->band_bits, c->n_bands);
-                else
+                if (!c->staged) {     // the staged path's keys were written when the queue was pushed
                     k_sort_keys<false><<<grid_for(nL, BLK, 1 << 30), BLK, 0, st>>>(
-                        cur, (int32_t)nL, c->ps_cur, c->L, c->keys_in.p, c->ebin_bits, c->ebin_shift, c->mat_bits,
+                        cur, (int32_t)nL, c->ps_cur, c->L, kcur, c->ebin_bits, c->ebin_shift, c->mat_bits,
                         c->band_bits, c->n_bands);
-                EMC_CHECK_LAUNCH(c);
-                int rc = sort_cub(c, c->keys_in.p, c->keys_out.p, cur, c->qs.p, (int)nL, c->key_bits);
+                    EMC_CHECK_LAUNCH(c);
+                }
+                int rc = sort_cub(c, kcur, c->keys_out.p, cur, c->qs.p, (int)nL, c->key_bits);
                 if (rc) return rc;
                 q = c->qs.p;
                 host_cnt[CNT_SORTS] += 1;
@@ -798,16 +802,18 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             EMC_CHECK_LAUNCH(c);
             EMC_TRY_CUDA(cudaEventRecord(c->ev[2], st));
             k_advance<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(q, (int32_t)nL, bp, c->L, c->G, c->S, lg, c->bins.p,
-                                                              c->qc.p, c->qx.p, c->ctl.p, c->cnt.p, c->M, nullptr, nxt);
+                                                              c->qc.p, c->qx.p, c->ctl.p, c->cnt.p, c->M, nullptr, nxt,
+                                                              qk(knxt));
             EMC_CHECK_LAUNCH(c);
             if (c->G.vacuum) {       // leakage: end and refill (reflective problems cross inside k_advance)
                 k_crossing<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(c->qx.p, &c->ctl.p->nX, bp, c->L, c->G, c->src,
-                                                                   c->S, nxt, c->ctl.p, c->cnt.p);
+                                                                   c->S, nxt, c->ctl.p, c->cnt.p, qk(knxt));
                 EMC_CHECK_LAUNCH(c);
             }
             EMC_TRY_CUDA(cudaEventRecord(c->ev[3], st));
             k_collision<<<grid_for(nL, BLK, maxb), BLK, 0, st>>>(c->qc.p, &c->ctl.p->nC, bp, c->L, c->G, c->src,
-                                                                c->S, lg, sv, c->bins.p, nxt, c->ctl.p, c->cnt.p);
+                                                                c->S, lg, sv, c->bins.p, nxt, c->ctl.p, c->cnt.p,
+                                                                qk(knxt));
             EMC_CHECK_LAUNCH(c);
             EMC_TRY_CUDA(cudaEventRecord(c->ev[4], st));
             EMC_TRY_CUDA(cudaMemcpyAsync(c->ctl_host, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
@@ -822,6 +828,7 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             host_cnt[CNT_MAX_INFLIGHT] = std::max(host_cnt[CNT_MAX_INFLIGHT], nL);
             nL = c->ctl_host->nL2;
             std::swap(cur, nxt);
+            std::swap(kcur, knxt);
             iterations++;
         }
     }

@@ -32,6 +32,43 @@ namespace emc {
                  emc_stride_ = (int64_t)gridDim.x * blockDim.x;                            \
          emc_base_ < (int64_t)(n); emc_base_ += emc_stride_)
 
+// queue_push that also stores the lookup sort key at the pushed position
+__device__ __forceinline__ void queue_push_key(int32_t* q, unsigned int* count, int32_t slot, bool pred,
+                                               uint32_t* keys, uint32_t key)
+{
+    unsigned int mask = __ballot_sync(kFull, pred);
+    unsigned int rank = __popc(mask & ((1u << lane_id()) - 1u));
+    unsigned int base = 0;
+    if (lane_id() == 0 && mask) base = atomicAdd(count, (unsigned int)__popc(mask));
+    base = __shfl_sync(kFull, base, 0);
+    if (pred) {
+        q[base + rank] = slot;
+        if (keys) keys[base + rank] = key;
+    }
+}
+
+// Lookup-queue sort keys written at push time (energy-major key of
+// k_sort_keys<true>): the kernels that put a particle on the next lookup
+// queue know its energy and material, so the sort needs no separate gather
+// pass over the particle lines.  keys == nullptr: not written.
+struct QKeys {
+    uint32_t* keys;
+    int32_t ebin_bits, ebin_shift, mat_bits, fine_bits;
+};
+
+__device__ __forceinline__ uint32_t lookup_key(const DLib& L, const QKeys& K, double E, int32_t m)
+{
+    const uint32_t eb = (uint32_t)energy_bin(E, L);
+    uint32_t k = (uint32_t)__ldg(L.mat_group + m);
+    k = K.ebin_bits ? ((k << K.ebin_bits) | (eb >> K.ebin_shift)) : k;
+    k = (k << K.mat_bits) | (uint32_t)m;
+    if (K.fine_bits) {
+        const uint64_t e64 = (uint64_t)__double_as_longlong(E);
+        k = (k << K.fine_bits) | (uint32_t)((e64 >> (L.shift - K.fine_bits)) & ((1u << K.fine_bits) - 1u));
+    }
+    return k;
+}
+
 // ----------------------------------------------------------- sourcing ---
 
 // systematic resampling index of particle g (transport.py:188-200)
@@ -114,17 +151,19 @@ __device__ __forceinline__ bool source_particle(int32_t slot, int64_t g, const B
 }
 
 __global__ void k_source_init(BatchP bp, DLib L, DGeom G, DSrc src, DSlots S, int32_t n0,
-                              int32_t* q, Ctl* ctl, unsigned long long* cnt)
+                              int32_t* q, Ctl* ctl, unsigned long long* cnt, QKeys K)
 {
     int clamps = 0; unsigned long long sourced = 0;
     EMC_WARP_LOOP(n0) {
         int64_t i = emc_base_ + lane_id();
         bool ok = false;
+        uint32_t key = 0;
         if (i < n0) {
             ok = source_particle((int32_t)i, bp.g_lo + i, bp, L, G, src, S, ctl, clamps);
             sourced += 1;
+            if (ok && K.keys) key = lookup_key(L, K, S.ps[i].a.E, S.ps[i].d.mat);
         }
-        queue_push(q, &ctl->nL2, (int32_t)i, ok);
+        queue_push_key(q, &ctl->nL2, (int32_t)i, ok, K.keys, key);
     }
     warp_add_u64(cnt + CNT_SOURCED, sourced);
     warp_add_u64(cnt + CNT_CLAMPS, (unsigned long long)clamps);
@@ -343,7 +382,7 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
                                                  DLib L, DGeom G, DSlots S, DLog lg, double* bins,
                                                  int32_t* q_col, int32_t* q_cross, Ctl* ctl,
                                                  unsigned long long* cnt, DMesh M, const unsigned int* nptr,
-                                                 int32_t* q_next)
+                                                 int32_t* q_next, QKeys K)
 {
     if (nptr) n = (int32_t)*nptr;        // tail mode: queue length lives on the device
     unsigned long long interp_score = 0;
@@ -351,6 +390,7 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
         int64_t i = emc_base_ + lane_id();
         bool valid = i < n, to_col = false, to_cross = false, leak = false;
         int32_t s = valid ? q[i] : 0;
+        double kE = 1.0;                     // energy for the next lookup's sort key
         double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         int32_t base = 0;
         unsigned nlog = 0;
@@ -409,6 +449,7 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
                         to_cross = crossing;
                         leak = crossing && G.vacuum && surf >= SURF_XMIN && surf <= SURF_ZMAX;
                         if (crossing && !leak) cross_surface(a, b, d, G);
+                        kE = a.E;
                     }
                     p.a = a; p.b = b;
                 }
@@ -443,7 +484,9 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
         }
         if (to_col || to_cross) S.ps[s].d = d;
         queue_push(q_col, &ctl->nC, s, to_col);
-        queue_push(q_next, &ctl->nL2, s, to_cross && !leak);
+        const bool to_next = to_cross && !leak;
+        queue_push_key(q_next, &ctl->nL2, s, to_next, K.keys,
+                       (to_next && K.keys) ? lookup_key(L, K, kE, d.mat) : 0u);
         if (G.vacuum) queue_push(q_cross, &ctl->nX, s, to_cross && leak);
     }
     warp_add_u64(cnt + CNT_INTERP_SCORE, interp_score);
@@ -457,7 +500,7 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
 // and the slot is refilled from the batch cursor like a collision death.
 __global__ void __launch_bounds__(256, EMC_COL_MINB) k_crossing(const int32_t* __restrict__ q, const unsigned int* nq,
                                                   BatchP bp, DLib L, DGeom G, DSrc src, DSlots S, int32_t* q_next,
-                                                  Ctl* ctl, unsigned long long* cnt)
+                                                  Ctl* ctl, unsigned long long* cnt, QKeys K)
 {
     const int32_t n = (int32_t)*nq;
     unsigned long long leaks = 0, sourced = 0, maxdraws = 0, maxhist = 0;
@@ -488,7 +531,9 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_crossing(const int32_t* _
                 sourced += 1;
             }
         }
-        queue_push(q_next, &ctl->nL2, s, (valid && !died) || refill);
+        const bool nxt = (valid && !died) || refill;
+        queue_push_key(q_next, &ctl->nL2, s, nxt, K.keys,
+                       (nxt && K.keys) ? lookup_key(L, K, S.ps[s].a.E, S.ps[s].d.mat) : 0u);
     }
     if (G.vacuum) {
         warp_add_u64(cnt + CNT_LEAKS, leaks);
@@ -598,7 +643,7 @@ __device__ __forceinline__ int32_t select_nuclide(const DLib& L, const double* c
 __global__ void __launch_bounds__(256, EMC_COL_MINB) k_collision(const int32_t* __restrict__ q, const unsigned int* nq,
                                                    BatchP bp, DLib L, DGeom G, DSrc src, DSlots S,
                                                    DLog lg, DSites sb, double* bins, int32_t* q_next,
-                                                   Ctl* ctl, unsigned long long* cnt)
+                                                   Ctl* ctl, unsigned long long* cnt, QKeys K)
 {
     const int32_t n = (int32_t)*nq;
     unsigned long long interp = 0, captures = 0, fissions = 0, sourced = 0;
@@ -699,7 +744,10 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_collision(const int32_t* 
             refill = source_particle(s, bp.g_lo + (int64_t)idx, bp, L, G, src, S, ctl, clamps);
             sourced += 1;
         }
-        queue_push(q_next, &ctl->nL2, s, alive || refill);
+        const bool nxt = alive || refill;
+        queue_push_key(q_next, &ctl->nL2, s, nxt, K.keys,
+                       !(nxt && K.keys) ? 0u : alive ? lookup_key(L, K, a.E, d.mat)
+                                                     : lookup_key(L, K, S.ps[s].a.E, S.ps[s].d.mat));
     }
     warp_add_u64(cnt + CNT_INTERP_TRANSPORT, interp);
     warp_add_u64(cnt + CNT_CAPTURES, captures);
