@@ -176,6 +176,7 @@ struct emc_ctx {
     // tail mode (EMC_TAIL_N, EMC_TAIL_K): queues below tail_n once the source is
     // exhausted run tail_k iterations per host round trip, unsorted
     int64_t tail_n = 262144;
+    bool trace = getenv("EMC_TRACE") != nullptr;   // per-iteration queue length / lookup time on stderr
     int tail_k = 16;
     cudaEvent_t evt[4 * 32]{};
     bool ev_init = false;
@@ -820,6 +821,8 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             EMC_TRY_CUDA(cudaStreamSynchronize(st));
             cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]); tm[3] += ms * 1e-3;
             cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]); tm[0] += ms * 1e-3;
+            if (c->trace) std::fprintf(stderr, "emc-trace iter %lld nL %lld lookup_ms %.4f\n", (long long)iterations,
+                                       (long long)nL, ms);
             cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]); tm[1] += ms * 1e-3;
             cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]); tm[2] += ms * 1e-3;
             int64_t nC = c->ctl_host->nC;

@@ -92,6 +92,7 @@ class DeviceEngine:
         desc = N.EmcGeometry(radius, r2, hp, height, int(n_axial), N.ptr(zp), N.ptr(fm),
                              int(mod_mat))
         N.check(self.lib.emc_upload_geometry(self._h, C.byref(desc)), "emc_upload_geometry")
+        self._geometry_options(pincell)
         self.pincell_obj = weakref.ref(pincell)
         self.n_bins = (int(n_axial) + 1) * 5 + 1
 
@@ -105,17 +106,23 @@ class DeviceEngine:
                              config.fission_temperature, int(config.perturb_particle))
         N.check(self.lib.emc_configure(self._h, C.byref(cfg)), "emc_configure")
 
-    def set_extensions(self, pincell, config) -> None:
-        """Slab/vacuum geometry, fixed source and mesh tally (extensions,
-        SURVEY 8f row 1); applied on every run because engines are reused."""
+    def _geometry_options(self, pincell) -> None:
+        """Slab / vacuum / lattice (extensions): part of
+        the geometry, so every upload applies them (off for the reference's
+        pincell)."""
         N.check(self.lib.emc_set_geometry_options(self._h, int(pincell.is_slab),
                                                   int(pincell.boundary == "vacuum")),
                 "emc_set_geometry_options")
-        N.check(self.lib.emc_set_fixed_source(self._h, int(config.run_mode == "fixed_source"),
-                                              float(config.source_energy)), "emc_set_fixed_source")
         n = int(getattr(pincell, "lattice", 1))
         pm = np.ascontiguousarray(pincell.pin_map if n > 1 else [1], np.int32)
         N.check(self.lib.emc_set_lattice(self._h, n, float(pincell.pitch), N.ptr(pm)), "emc_set_lattice")
+
+    def set_extensions(self, pincell, config) -> None:
+        """Geometry options, fixed source and mesh tally (extensions, SURVEY
+        8f); applied on every run because engines are reused."""
+        self._geometry_options(pincell)
+        N.check(self.lib.emc_set_fixed_source(self._h, int(config.run_mode == "fixed_source"),
+                                              float(config.source_energy)), "emc_set_fixed_source")
         nx, ny, nz = (int(v) for v in config.mesh) if config.mesh is not None else (0, 0, 0)
         N.check(self.lib.emc_set_mesh(self._h, nx, ny, nz), "emc_set_mesh")
 

@@ -159,3 +159,43 @@ def test_edge_library_staged_paths_match_oracle(cap):
     ores = driver.run(dict(cfg.__dict__), lib.arrays(), cell.as_tuple())
     assert res.physics_fingerprint() == driver.fingerprint(ores)
     assert res.counters["interp_transport"] == ores["counters"]["interp_transport"]
+
+
+@pytest.mark.parametrize("which", ["lattice", "slab", "pincell_vacuum"])
+def test_extension_geometry_ops_match_oracle(which):
+    """Cell search and distance-to-boundary of the extension geometries on the
+    device (public API) against the oracle, bit for bit, on random points and
+    directions, including points near lattice planes and pin surfaces."""
+    from paper_2403_12345_b200.engine import api_engine
+    if which == "lattice":
+        _, cell = P.pwr_assembly(gridpoints=50)
+        og = driver.OracleGeometry(cell.as_tuple(), lattice=(cell.lattice, cell.pitch, cell.pin_map))
+    elif which == "slab":
+        _, cell = P.shielding_slab(gridpoints=50)
+        og = driver.OracleGeometry(cell.as_tuple(), slab=True, vacuum=True)
+    else:
+        cell = P.Pincell(n_axial=4, fuel_material_ids=[0, 0, 0, 0], moderator_material_id=0, boundary="vacuum")
+        og = driver.OracleGeometry(cell.as_tuple(), vacuum=True)
+    rng = np.random.default_rng(17)
+    n = 6000
+    hp, h = cell.half_width, cell.height
+    pts = np.stack([rng.uniform(-hp, hp, n), rng.uniform(-hp, hp, n), rng.uniform(0, h, n)], 1)
+    if which == "lattice":      # cluster a third of the points on cell planes and pin surfaces
+        k = n // 3
+        i = rng.integers(0, cell.lattice, k)
+        pts[:k, 0] = -hp + i * cell.pitch + rng.normal(0, 1e-9, k)
+        ang = rng.uniform(0, 2 * np.pi, k)
+        pts[k:2 * k, 0] = -hp + (rng.integers(0, 17, k) + 0.5) * cell.pitch + cell.fuel_radius * np.cos(ang)
+        pts[k:2 * k, 1] = -hp + (rng.integers(0, 17, k) + 0.5) * cell.pitch + cell.fuel_radius * np.sin(ang)
+    mu = rng.uniform(-1, 1, n)
+    phi = rng.uniform(0, 2 * np.pi, n)
+    dirs = np.stack([np.sqrt(1 - mu * mu) * np.cos(phi), np.sqrt(1 - mu * mu) * np.sin(phi), mu], 1)
+    loc = P.geometry.locate_batch(cell, pts)
+    want = np.array([driver.locate(og, *p) for p in pts])
+    assert np.array_equal(loc, want)
+    inside = loc[:, 0] >= 0
+    cells = loc[inside][:, :2].astype(np.int32)
+    dist, surf = api_engine(pincell=cell).distance(pts[inside], dirs[inside], cells)
+    for j, (p, d, c) in enumerate(zip(pts[inside], dirs[inside], cells)):
+        od, osf = driver.boundary_distance(og, p, d, int(c[0]), int(c[1]))
+        assert (dist[j], surf[j]) == (od, osf), (j, p, d, c)
