@@ -250,7 +250,11 @@ __device__ __forceinline__ void lk_prefetch(const DLib& L, int32_t e0, int32_t k
 // MODE 0: transport (queue q of slots, writes PState.c and the sigma_t
 //         checkpoints); MODE 1: microbenchmark over (bE, bM), writes
 //         bout[i] = st + sc + sf + snf and checkpoints at bout + n.
-template <int MODE, bool DEN_ST, int NW, int MINB>
+// PPL particles per consumer lane (adjacent queue entries): the stage's meta
+// word, window energies and control flow are shared by the lane's particles,
+// and their independent folds give the scheduler instruction-level
+// parallelism to cover the shared-memory latency.
+template <int MODE, bool DEN_ST, int NW, int MINB, int PPL>
 __global__ void __launch_bounds__(NW * 32, MINB)
     k_lookup_staged(const int32_t* __restrict__ q, int32_t n, DLib L, DSlots S, int32_t fused,
                     unsigned long long* cnt, const double* __restrict__ bE, const int32_t* __restrict__ bM,
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     LkShared& sh = *reinterpret_cast<LkShared*>(lk_raw);
     double* const sden = reinterpret_cast<double*>(lk_raw + sizeof(LkShared));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int LK_CONS = NW - 1, LK_CHUNK = LK_CONS * 32;
+    constexpr int LK_CONS = NW - 1, LK_CHUNK = LK_CONS * 32 * PPL;
     const bool producer = warp == LK_CONS;
     const int32_t nmat = L.n_mat;
     const int32_t nck = MODE == 0 ? S.nck : 16;
@@ -278,59 +282,81 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     uint32_t T = 0;                 // pipeline stage counter, identical in every thread
     unsigned long long nl = 0;
     for (int64_t base = (int64_t)blockIdx.x * LK_CHUNK; base < n; base += (int64_t)gridDim.x * LK_CHUNK) {
-        const int64_t i = base + threadIdx.x;
-        bool pend = !producer && i < n;
-        int32_t s = 0, m = 0, grp = 0, bin = 0;
-        double E = 1.0;
-        if (pend) {
-            if (MODE == 0 && rdst) {
-                // fused reorder (replaces k_reorder): move the particle's line to
-                // queue position i, which becomes its slot from here on
-                const PState line = S.ps[q[i]];
-                rdst[i] = line;
-                s = (int32_t)i;
-                E = line.a.E;
-                m = line.d.mat;
-            } else if (MODE == 0) {
-                s = q[i];
-                E = S.ps[s].a.E;
-                m = S.ps[s].d.mat;
-            } else {
-                E = bE[i];
-                m = bM[i];
+        int64_t i[PPL];
+        bool pend[PPL];
+        int32_t s[PPL], m[PPL], grp[PPL], bin[PPL];
+        double E[PPL];
+#pragma unroll
+        for (int p = 0; p < PPL; ++p) {
+            i[p] = base + (int64_t)threadIdx.x * PPL + p;
+            pend[p] = !producer && i[p] < n;
+            s[p] = 0; m[p] = 0; grp[p] = 0; bin[p] = 0; E[p] = 1.0;
+            if (pend[p]) {
+                if (MODE == 0 && rdst) {
+                    // fused reorder (replaces k_reorder): move the particle's line to
+                    // queue position i, which becomes its slot from here on
+                    const PState line = S.ps[q[i[p]]];
+                    rdst[i[p]] = line;
+                    s[p] = (int32_t)i[p];
+                    E[p] = line.a.E;
+                    m[p] = line.d.mat;
+                } else if (MODE == 0) {
+                    s[p] = q[i[p]];
+                    E[p] = S.ps[s[p]].a.E;
+                    m[p] = S.ps[s[p]].d.mat;
+                } else {
+                    E[p] = bE[i[p]];
+                    m[p] = bM[i[p]];
+                }
+                grp[p] = __ldg(L.mat_group + m[p]);
+                bin[p] = energy_bin(E[p], L);
             }
-            grp = __ldg(L.mat_group + m);
-            bin = energy_bin(E, L);
         }
         // one pass per composition group present in the chunk (normally one)
         for (;;) {
             if (threadIdx.x == 0) { sh.grp = INT32_MAX; sh.bmin = INT32_MAX; sh.bmax = -1; }
             __syncthreads();
             {
-                const int g = warp_min_i32(pend ? grp : INT32_MAX);
+                int g = INT32_MAX;
+#pragma unroll
+                for (int p = 0; p < PPL; ++p) g = min(g, pend[p] ? grp[p] : INT32_MAX);
+                g = warp_min_i32(g);
                 if (lane == 0 && g != INT32_MAX) atomicMin(&sh.grp, g);
             }
             __syncthreads();
             const int32_t G = sh.grp;
             if (G == INT32_MAX) break;
-            const bool mine = pend && grp == G;
+            bool mine[PPL], any = false;
             {
-                const int b0 = warp_min_i32(mine ? bin : INT32_MAX), b1 = warp_max_i32(mine ? bin : -1);
+                int b0 = INT32_MAX, b1 = -1;
+#pragma unroll
+                for (int p = 0; p < PPL; ++p) {
+                    mine[p] = pend[p] && grp[p] == G;
+                    any |= mine[p];
+                    if (mine[p]) { b0 = min(b0, bin[p]); b1 = max(b1, bin[p]); }
+                }
+                b0 = warp_min_i32(b0);
+                b1 = warp_max_i32(b1);
                 if (lane == 0 && b1 >= 0) { atomicMin(&sh.bmin, b0); atomicMax(&sh.bmax, b1); }
             }
             __syncthreads();
             const int32_t bmin = sh.bmin, bmax = sh.bmax;
             const int32_t e0 = __ldg(L.grp_off + G), ncomp = __ldg(L.grp_off + G + 1) - e0;
-            double st = 0.0, sc = 0.0, sf = 0.0, snf = 0.0;
-            // sigma_t checkpoints: row r of this particle at ckb[r * cks] (formed
-            // at the store, not kept live through the nuclide loop)
+            double st[PPL], sc[PPL], sf[PPL], snf[PPL];
+#pragma unroll
+            for (int p = 0; p < PPL; ++p) { st[p] = 0.0; sc[p] = 0.0; sf[p] = 0.0; snf[p] = 0.0; }
+            // sigma_t checkpoints: row r of particle p at ckb[r * cks] (formed at
+            // the store, not kept live through the nuclide loop)
             const bool ckon = MODE == 1 || fused;
             const int64_t cks = MODE == 0 ? S.nslots : (int64_t)n;
             const int nst = (ncomp + LK_G - 1) / LK_G;
 
             if (ncomp < LK_MIN_NUC) {
-                if (mine) macro_tcf(L, m, E, st, sc, sf, snf,
-                                    ckon ? (MODE == 0 ? S.ckpt + s : bout + n + i) : nullptr, nck, cks);
+#pragma unroll
+                for (int p = 0; p < PPL; ++p)
+                    if (mine[p])
+                        macro_tcf(L, m[p], E[p], st[p], sc[p], sf[p], snf[p],
+                                  ckon ? (MODE == 0 ? S.ckpt + s[p] : bout + n + i[p]) : nullptr, nck, cks);
             } else if (producer) {
                 // lane j < LK_G owns nuclide 8t+j of every stage; its global
                 // reads for stage t+1 are issued before it waits for slot t
@@ -360,65 +386,96 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                                  (uint32_t)lk_den_block(nmat), &sh.full[d]);
                 }
             } else {
+                // a lane's particles outside this pass's group compute on a copy
+                // of a member's (energy, bin, material) -- their windows would
+                // not hold their brackets -- and their results are discarded
+                double Eu[PPL];
+                int32_t bu[PPL], mu[PPL];
+                {
+                    int32_t pm = 0;
+#pragma unroll
+                    for (int p = PPL - 1; p >= 0; --p) if (mine[p]) pm = p;
+#pragma unroll
+                    for (int p = 0; p < PPL; ++p) {
+                        Eu[p] = mine[p] ? E[p] : E[pm];
+                        bu[p] = mine[p] ? bin[p] : bin[pm];
+                        mu[p] = mine[p] ? m[p] : m[pm];
+                    }
+                }
                 for (int t = 0; t < nst; ++t, ++T) {
                     const int d = (int)(T % LK_D);
                     mbar_wait(&sh.full[d], (T / LK_D) & 1);
-                    if (mine) {
-                        const double* dens = DEN_ST ? sden + ((size_t)d * nmat + m) * LK_DS : nullptr;
+                    if (any) {
 #pragma unroll
                         for (int j = 0; j < LK_G; ++j) {
                             const int k = t * LK_G + j;
                             if (k >= ncomp) break;
-                            const double2 dd = DEN_ST ? *reinterpret_cast<const double2*>(dens + 2 * j)
-                                                      : *reinterpret_cast<const double2*>(&L.ddT[(int64_t)k * nmat + m]);
-                            const double den = dd.x, dn = dd.y;
                             const uint32_t wd = sh.word[d][j];
                             const IvRec* W = sh.iv[d][j];
                             // issued with the meta word (always in-bounds shared memory)
                             const double a1 = W[1].E0, a2 = W[2].E0;
-                            double tt, cc, ff;
+                            double tt[PPL], cc[PPL], ff[PPL];
                             if (__builtin_expect(wd <= 4u, 1)) {
                                 // <= 3 interior intervals: li = #{j in 1..cnt-2 : E0_j <= E}
                                 // (grids ascend; entries past the window are stale, hence
                                 // the clamp to cnt-2).  Away from the grid ends E lies in
                                 // [E0, E1) of interval li: no clamp can apply.
-                                const int32_t li = min((int32_t)(a1 <= E) + (int32_t)(a2 <= E), (int32_t)wd - 2);
-                                const double2 er = *reinterpret_cast<const double2*>(&W[li].E0);   // (E0, r)
-                                const double e1 = W[li + 1].E0;
-                                const IvRec& a = W[li];
-                                const double fr = div_by_rcp_safe(__dsub_rn(E, er.x), __dsub_rn(e1, er.x), er.y);
-                                tt = __dadd_rn(a.t0, __dmul_rn(fr, a.dt));
-                                cc = __dadd_rn(a.c0, __dmul_rn(fr, a.dc));
-                                ff = __dadd_rn(a.f0, __dmul_rn(fr, a.df));
+#pragma unroll
+                                for (int p = 0; p < PPL; ++p) {
+                                    const int32_t li =
+                                        min((int32_t)(a1 <= Eu[p]) + (int32_t)(a2 <= Eu[p]), (int32_t)wd - 2);
+                                    const double2 er = *reinterpret_cast<const double2*>(&W[li].E0);   // (E0, r)
+                                    const double e1 = W[li + 1].E0;
+                                    const IvRec& a = W[li];
+                                    const double fr =
+                                        div_by_rcp_safe(__dsub_rn(Eu[p], er.x), __dsub_rn(e1, er.x), er.y);
+                                    tt[p] = __dadd_rn(a.t0, __dmul_rn(fr, a.dt));
+                                    cc[p] = __dadd_rn(a.c0, __dmul_rn(fr, a.dc));
+                                    ff[p] = __dadd_rn(a.f0, __dmul_rn(fr, a.df));
+                                }
                             } else {
-                                lk_micro_slow(L, sh.meta[d][j], wd, W, a1, a2, bin, E, tt, cc, ff);
+#pragma unroll
+                                for (int p = 0; p < PPL; ++p)
+                                    lk_micro_slow(L, sh.meta[d][j], wd, W, a1, a2, bu[p], Eu[p], tt[p], cc[p], ff[p]);
                             }
-                            st = __dadd_rn(st, __dmul_rn(den, tt));
-                            sc = __dadd_rn(sc, __dmul_rn(den, cc));
-                            sf = __dadd_rn(sf, __dmul_rn(den, ff));
-                            snf = __dadd_rn(snf, __dmul_rn(dn, ff));
+#pragma unroll
+                            for (int p = 0; p < PPL; ++p) {
+                                const double2 dd =
+                                    DEN_ST ? *reinterpret_cast<const double2*>(sden + ((size_t)d * nmat + mu[p]) * LK_DS + 2 * j)
+                                           : *reinterpret_cast<const double2*>(&L.ddT[(int64_t)k * nmat + mu[p]]);
+                                st[p] = __dadd_rn(st[p], __dmul_rn(dd.x, tt[p]));
+                                sc[p] = __dadd_rn(sc[p], __dmul_rn(dd.x, cc[p]));
+                                sf[p] = __dadd_rn(sf[p], __dmul_rn(dd.x, ff[p]));
+                                snf[p] = __dadd_rn(snf[p], __dmul_rn(dd.y, ff[p]));
+                            }
                         }
                         // prefix checkpoint after every kCkptStride (= 2 stages) nuclides
                         static_assert(kCkptStride == 2 * LK_G, "checkpoint every second stage");
                         if (ckon && (t & 1) && (t + 1) * LK_G <= ncomp) {
                             const int32_t row = t >> 1;
-                            double* ckb = MODE == 0 ? S.ckpt + s : bout + n + i;
-                            if (row < nck) ckb[(int64_t)row * cks] = st;
+#pragma unroll
+                            for (int p = 0; p < PPL; ++p) {
+                                double* ckb = MODE == 0 ? S.ckpt + s[p] : bout + n + i[p];
+                                if (mine[p] && row < nck) ckb[(int64_t)row * cks] = st[p];
+                            }
                         }
                     }
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&sh.empty[d]);
                 }
             }
-            if (mine) {
-                if (MODE == 0) {
-                    P2 c; c.t = st; c.c = sc; c.f = sf; c.nsf = snf;
-                    (rdst ? rdst : S.ps)[s].c = c;
-                } else {
-                    bout[i] = st + sc + sf + snf;
+#pragma unroll
+            for (int p = 0; p < PPL; ++p) {
+                if (mine[p]) {
+                    if (MODE == 0) {
+                        P2 c; c.t = st[p]; c.c = sc[p]; c.f = sf[p]; c.nsf = snf[p];
+                        (rdst ? rdst : S.ps)[s[p]].c = c;
+                    } else {
+                        bout[i[p]] = st[p] + sc[p] + sf[p] + snf[p];
+                    }
+                    nl += (unsigned long long)ncomp;
+                    pend[p] = false;
                 }
-                nl += (unsigned long long)ncomp;
-                pend = false;
             }
             __syncthreads();
         }
@@ -433,11 +490,13 @@ __global__ void __launch_bounds__(NW * 32, MINB)
 
 namespace emc {
 
-// Launch configurations of the staged lookup (warps per CTA x CTAs per SM).
-// EMC_LK_CFG selects one at run time (tuning); 0 is the default.
-constexpr int LK_NCFG = 3;
-constexpr int lk_cfg_warps(int c) { return c == 1 ? 20 : c == 2 ? 16 : 32; }
-constexpr int lk_cfg_minb(int c) { return c == 0 ? 1 : 2; }
+// Launch configurations of the staged lookup (warps per CTA x CTAs per SM x
+// particles per lane).  EMC_LK_CFG selects one at run time (tuning); 0 is
+// the default.
+constexpr int LK_NCFG = 4;
+constexpr int lk_cfg_warps(int c) { return c == 1 ? 20 : c == 2 ? 16 : c == 3 ? 17 : 32; }
+constexpr int lk_cfg_minb(int c) { return c == 1 || c == 2 ? 2 : 1; }
+constexpr int lk_cfg_ppl(int c) { return c == 3 ? 2 : 1; }
 
 template <int MODE, int CFG>
 inline cudaError_t lk_launch_cfg(const DLib& L, const int32_t* q, int64_t n, DSlots S, int32_t fused,
@@ -445,15 +504,15 @@ inline cudaError_t lk_launch_cfg(const DLib& L, const int32_t* q, int64_t n, DSl
                                  int sm_count, size_t smem, cudaStream_t st, const unsigned int* nptr,
                                  PState* rdst)
 {
-    constexpr int NW = lk_cfg_warps(CFG), MB = lk_cfg_minb(CFG);
-    constexpr int64_t chunk = (NW - 1) * 32;
+    constexpr int NW = lk_cfg_warps(CFG), MB = lk_cfg_minb(CFG), PP = lk_cfg_ppl(CFG);
+    constexpr int64_t chunk = (NW - 1) * 32 * PP;
     const unsigned nb = (unsigned)std::min<int64_t>((n + chunk - 1) / chunk, (int64_t)sm_count * MB);
     if (L.den_staged)
-        k_lookup_staged<MODE, true, NW, MB><<<nb, NW * 32, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM, bout,
-                                                                       nptr, rdst);
+        k_lookup_staged<MODE, true, NW, MB, PP><<<nb, NW * 32, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM,
+                                                                           bout, nptr, rdst);
     else
-        k_lookup_staged<MODE, false, NW, MB><<<nb, NW * 32, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM,
-                                                                        bout, nptr, rdst);
+        k_lookup_staged<MODE, false, NW, MB, PP><<<nb, NW * 32, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM,
+                                                                            bout, nptr, rdst);
     return cudaGetLastError();
 }
 
@@ -466,6 +525,7 @@ inline cudaError_t lk_launch(int cfg, const DLib& L, const int32_t* q, int64_t n
     switch (cfg) {
     case 1: return lk_launch_cfg<MODE, 1>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, nptr, rdst);
     case 2: return lk_launch_cfg<MODE, 2>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, nptr, rdst);
+    case 3: return lk_launch_cfg<MODE, 3>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, nptr, rdst);
     default: return lk_launch_cfg<MODE, 0>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, nptr, rdst);
     }
 }
@@ -473,11 +533,11 @@ inline cudaError_t lk_launch(int cfg, const DLib& L, const int32_t* q, int64_t n
 template <int MODE, int CFG>
 inline cudaError_t lk_set_smem_cfg(size_t smem)
 {
-    constexpr int NW = lk_cfg_warps(CFG), MB = lk_cfg_minb(CFG);
-    cudaError_t e = cudaFuncSetAttribute(k_lookup_staged<MODE, true, NW, MB>,
+    constexpr int NW = lk_cfg_warps(CFG), MB = lk_cfg_minb(CFG), PP = lk_cfg_ppl(CFG);
+    cudaError_t e = cudaFuncSetAttribute(k_lookup_staged<MODE, true, NW, MB, PP>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_lookup_staged<MODE, false, NW, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(k_lookup_staged<MODE, false, NW, MB, PP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)smem);
 }
 
@@ -485,7 +545,8 @@ inline cudaError_t lk_set_smem(size_t smem)
 {
     cudaError_t e;
     if ((e = lk_set_smem_cfg<0, 0>(smem)) || (e = lk_set_smem_cfg<0, 1>(smem)) || (e = lk_set_smem_cfg<0, 2>(smem)) ||
-        (e = lk_set_smem_cfg<1, 0>(smem)) || (e = lk_set_smem_cfg<1, 1>(smem)) || (e = lk_set_smem_cfg<1, 2>(smem)))
+        (e = lk_set_smem_cfg<0, 3>(smem)) || (e = lk_set_smem_cfg<1, 0>(smem)) || (e = lk_set_smem_cfg<1, 1>(smem)) ||
+        (e = lk_set_smem_cfg<1, 2>(smem)) || (e = lk_set_smem_cfg<1, 3>(smem)))
         return e;
     return cudaSuccess;
 }
