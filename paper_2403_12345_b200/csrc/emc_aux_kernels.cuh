@@ -20,6 +20,17 @@ __global__ void k_bank_keys(const int64_t* __restrict__ parent, const int32_t* _
     idx[i] = (int32_t)i;
 }
 
+// 32-bit (parent - g_lo, ordinal) keys when they fit (see emc_engine.cu)
+__global__ void k_bank_keys32(const int64_t* __restrict__ parent, const int32_t* __restrict__ ord,
+                              int64_t n, int64_t g_lo, int ord_bits, uint32_t* __restrict__ keys,
+                              int32_t* __restrict__ idx)
+{
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    keys[i] = ((uint32_t)(parent[i] - g_lo) << ord_bits) | (uint32_t)ord[i];
+    idx[i] = (int32_t)i;
+}
+
 __global__ void k_bank_gather(const int32_t* __restrict__ idx, int64_t n, DSites in, DSites out)
 {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -115,6 +115,7 @@ struct emc_ctx {
     int32_t n_groups = 0;
     DLib L{};
     int32_t n_materials = 0, max_comp = 0;
+    double nu_max = 0.0;         // largest nu of the library (bounds the fission-site ordinal)
     int64_t lib_bytes = 0;
 
     // geometry
@@ -392,6 +393,8 @@ extern "C" int emc_upload_library(emc_ctx* c, const emc_library* lib)
     if (const char* lc = getenv("EMC_LK_CFG")) c->lk_cfg = std::max(0, std::min(LK_NCFG - 1, atoi(lc)));
     c->n_materials = (int32_t)nm;
     c->max_comp = maxc;
+    c->nu_max = 0.0;
+    for (int64_t i = 0; i < nn; ++i) c->nu_max = std::max(c->nu_max, lib->nu[i]);
     c->lib_bytes = (int64_t)(np * (sizeof(Rec) + 8) + hcomp.size() * sizeof(Comp) + hhash.size() * 4);
     c->have_lib = true;
     return 0;
@@ -534,6 +537,8 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
     // fission bank: reference starts at n_assigned*6+1024 (R:92); ~1 site per
     // source particle is typical, so start at 2x and grow on overflow.
     if ((rc = alloc_sites(c, (size_t)(cfg->n_assigned * 2 + 4096)))) return rc;
+    // both canonical banks up front (a run starts without a live source bank)
+    if (c->banks[c->cur_bank].alloc(c->sites.parent.n)) return EMC_E_OOM;
     if (cfg->use_logs) {
         if ((rc = alloc_logs(c, (size_t)(cfg->n_assigned * 64 + 4096)))) return rc;
     }
@@ -569,12 +574,19 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
     int bb = 1;
     while ((1 << bb) < c->n_bins) ++bb;
     if (bb + gidb + 17 > 64) { g_err = "deterministic log key exceeds 64 bits"; return EMC_E_RANGE; }
-    // CUB scratch, sized for the largest sort we run
-    size_t t1 = 0, t2 = 0;
+    // CUB scratch, sized up front for the largest sorts we run (queue keys over
+    // the slots; 32- and 64-bit bank keys over the site capacity), so no batch
+    // pays a mid-run reallocation
+    size_t t1 = 0, t2 = 0, t3 = 0;
+    const int64_t scap = (int64_t)c->sites.parent.n;
     cub::DeviceRadixSort::SortPairs(nullptr, t1, (uint32_t*)nullptr, (uint32_t*)nullptr, (int32_t*)nullptr,
-                                    (int32_t*)nullptr, (int)nslots, 0, 32);
-    c->cub_tmp.alloc(std::max<size_t>(t1, 1));
-    (void)t2;
+                                    (int32_t*)nullptr, (int)std::max<int64_t>(nslots, scap), 0, 32);
+    cub::DeviceRadixSort::SortPairs(nullptr, t2, (uint64_t*)nullptr, (uint64_t*)nullptr, (int32_t*)nullptr,
+                                    (int32_t*)nullptr, (int)scap, 0, 64);
+    if (cfg->use_logs)
+        cub::DeviceRadixSort::SortPairs(nullptr, t3, (uint64_t*)nullptr, (uint64_t*)nullptr, (double*)nullptr,
+                                        (double*)nullptr, (int)c->lg_gid.n, 0, 64);
+    if (c->cub_tmp.alloc(std::max<size_t>(std::max(t1, std::max(t2, t3)), 1))) return EMC_E_OOM;
     c->bank_n = 0;
     c->src = DSrc{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.0, 0};
     c->configured = true;
@@ -699,11 +711,18 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
         auto qk = [&](uint32_t* k) {
             return QKeys{c->staged ? k : nullptr, c->ebin_bits, c->ebin_shift, c->mat_bits, c->band_bits};
         };
+        EMC_TRY_CUDA(cudaEventRecord(c->ev[5], st));
         k_source_init<<<grid_for(n0, BLK, maxb), BLK, 0, st>>>(bp, c->L, c->G, c->src, c->S, (int32_t)n0, cur,
                                                                c->ctl.p, c->cnt.p, qk(kcur));
         EMC_CHECK_LAUNCH(c);
+        EMC_TRY_CUDA(cudaEventRecord(c->ev[6], st));
         EMC_TRY_CUDA(cudaMemcpyAsync(c->ctl_host, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
         EMC_TRY_CUDA(cudaStreamSynchronize(st));
+        if (c->trace) {
+            float sm = 0;
+            cudaEventElapsedTime(&sm, c->ev[5], c->ev[6]);
+            std::fprintf(stderr, "emc-trace source_init_ms %.4f n0 %lld\n", sm, (long long)n0);
+        }
         int64_t nL = c->ctl_host->nL2;
         int64_t look_inv = 0, tail_blocks = 0;
         float ms;
@@ -898,18 +917,42 @@ extern "C" int emc_run_batch(emc_ctx* c, const emc_batch_args* a, emc_batch_resu
     // canonical bank: sort this rank's sites by (parent, ordinal)  (R:221-228)
     cudaStream_t st = c->stream;
     int64_t n = res->n_sites;
+    if (c->trace) EMC_TRY_CUDA(cudaEventRecord(c->ev[7], st));
     if (n > 0) {
         DSites sv = c->sites.view();
-        k_bank_keys<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(sv.parent, sv.ord, n, c->cfg.gid_lo, c->bkey_in.p,
-                                                               c->bidx_in.p);
-        EMC_CHECK_LAUNCH(c);
-        int kb = bits_for(c->cfg.n_assigned) + 20;
-        int rc = sort_cub64(c, c->bkey_in.p, c->bkey_out.p, c->bidx_in.p, c->bidx_out.p, n, kb);
+        // site ordinals are < floor(nu/k_run + u) + 1 <= nu_max/k_run + 2: when
+        // (parent, ordinal) fits 32 bits, sort 32-bit keys (fewer, narrower passes)
+        const double kr = a->k_run > 0.0 ? a->k_run : 1.0;
+        const double omax = std::floor(c->nu_max / kr) + 2.0;
+        const int ob = omax < 1048576.0 ? bits_for((int64_t)omax) : 20;
+        const int pb = bits_for(c->cfg.n_assigned);
+        int rc;
+        if (pb + ob <= 32) {
+            // the 64-bit key buffer (site capacity) holds both 32-bit key arrays
+            uint32_t* k32 = reinterpret_cast<uint32_t*>(c->bkey_in.p);
+            uint32_t* k32o = k32 + c->bkey_in.n;
+            k_bank_keys32<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(sv.parent, sv.ord, n, c->cfg.gid_lo, ob, k32,
+                                                                     c->bidx_in.p);
+            EMC_CHECK_LAUNCH(c);
+            rc = sort_cub(c, k32, k32o, c->bidx_in.p, c->bidx_out.p, (int)n, pb + ob);
+        } else {
+            k_bank_keys<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(sv.parent, sv.ord, n, c->cfg.gid_lo, c->bkey_in.p,
+                                                                   c->bidx_in.p);
+            EMC_CHECK_LAUNCH(c);
+            rc = sort_cub64(c, c->bkey_in.p, c->bkey_out.p, c->bidx_in.p, c->bidx_out.p, n, pb + 20);
+        }
         if (rc) return rc;
         SiteBufs& out = c->banks[1 - c->cur_bank];
         if (out.parent.n < (size_t)n && out.alloc(std::max<size_t>(n, c->sites.parent.n))) return EMC_E_OOM;
         k_bank_gather<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>(c->bidx_out.p, n, sv, out.view());
         EMC_CHECK_LAUNCH(c);
+    }
+    if (c->trace) {
+        EMC_TRY_CUDA(cudaEventRecord(c->ev[8], st));
+        EMC_TRY_CUDA(cudaEventSynchronize(c->ev[8]));
+        float bm = 0;
+        cudaEventElapsedTime(&bm, c->ev[7], c->ev[8]);
+        std::fprintf(stderr, "emc-trace bank_ms %.4f sites %lld\n", bm, (long long)n);
     }
     c->cur_bank = 1 - c->cur_bank;
     c->bank_n = n;
