@@ -70,7 +70,7 @@ def problem(args):
         return P.pwr_assembly()
     return P.depleted_pincell(272, 3, 11303, 100, seed=1)
 BYTES_PER_NUCLIDE_LOOKUP = 64
-TRAFFIC_PROFILE = "r1s3_lookup_traffic.json"
+TRAFFIC_PROFILE = "r1s4_lookup_traffic.json"
 
 
 def _peaks():
