@@ -188,10 +188,9 @@ int emc_libm_eval(emc_ctx *ctx, int64_t n, const double *x, double *out);
  * n/d correctly rounded; they must be equal bit for bit (parity test) */
 int emc_div_eval(emc_ctx *ctx, int64_t n, const double *num, const double *den, double *out);
 
-/* tuning harness: mean ms of the XS-lookup microbenchmark kernel over n
- * (material, energy) pairs; variant 0 = production arithmetic, 1-3 = timing
- * ablations (no division / shared energy / no gathers; wrong values), 4-7 =
- * plain-kernel variants, 8 = the shared-memory-staged production lookup */
+/* tuning harness: mean ms of a lookup kernel over n (material, energy)
+ * pairs: variant 8 = the shared-memory-staged production lookup, any other
+ * value = the plain gather lookup (macro_tcf) it replaced */
 int emc_bench_lookup(emc_ctx *ctx, int64_t n, const int32_t *mats, const double *E, int32_t variant,
                      int32_t iters, double *ms, double *checksum);
 

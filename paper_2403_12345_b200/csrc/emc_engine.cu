@@ -1258,20 +1258,11 @@ extern "C" int emc_bench_lookup(emc_ctx* c, int64_t n, const int32_t* mats, cons
     float total = 0;
     for (int it = 0; it <= iters; ++it) {
         EMC_TRY_CUDA(cudaEventRecord(c->ev[0], st));
-        switch (variant) {
-        case 1: k_lookup_bench<1><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
-        case 2: k_lookup_bench<2><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
-        case 3: k_lookup_bench<3><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
-        case 4: k_lookup_bench<4><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
-        case 5: k_lookup_bench<5><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
-        case 6: k_lookup_bench<6><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
-        case 7: k_lookup_bench<7><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p); break;
-        case 8: {
+        if (variant == 8) {
             EMC_TRY_CUDA(lk_launch<1>(c->lk_cfg, c->L, nullptr, n, c->S, 1, c->cnt.p, de.p, dm.p, dout.p, c->sm_count,
                                       c->lk_smem, st));
-            break;
-        }
-        default: k_lookup_bench<0><<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p);
+        } else {
+            k_lookup_bench<<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p);
         }
         EMC_CHECK_LAUNCH(c);
         EMC_TRY_CUDA(cudaEventRecord(c->ev[1], st));

@@ -234,9 +234,6 @@ __global__ void __launch_bounds__(256) k_reorder(const int32_t* __restrict__ per
 // block NT *consecutive* queue entries, so with NT = 1024 all 32 warps of an
 // SM work on neighbouring particles (same material, adjacent energies) and
 // share every grid record they gather through L1.
-#ifndef EMC_LOOKUP_PF
-#define EMC_LOOKUP_PF 0
-#endif
 template <int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_lookup(const int32_t* __restrict__ q, int32_t n, DLib L,
                                                         DSlots S, int32_t fused, unsigned long long* cnt)
@@ -249,11 +246,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_lookup(const int32_t* __restr
             double E = S.ps[s].a.E;
             int32_t m = S.ps[s].d.mat;
             P2 c;
-#if EMC_LOOKUP_PF
-            macro_tcf_pf(L, m, E, c.t, c.c, c.f, c.nsf, fused ? S.ckpt + s : nullptr, S.nck, S.nslots);
-#else
             macro_tcf(L, m, E, c.t, c.c, c.f, c.nsf, fused ? S.ckpt + s : nullptr, S.nck, S.nslots);
-#endif
             S.ps[s].c = c;
             nl += (unsigned long long)(__ldg(L.mat_off + m + 1) - __ldg(L.mat_off + m));
         }
@@ -262,63 +255,17 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_lookup(const int32_t* __restr
     warp_add_u64(cnt + CNT_NUCLIDE_LOOKUPS, nl);
 }
 
-// Lookup microbenchmark kernel (tools/lookup_micro.py via emc_bench_lookup):
-// VARIANT 0 = production arithmetic; 1 = no IEEE division (timing ablation);
-// 2 = every lane uses its warp's first energy (perfect record sharing);
-// 3 = no record gathers (synthetic records).  Variants 1-3 compute wrong
-// cross sections on purpose and are never used for transport.
-template <int VARIANT>
+// Lookup microbenchmark kernel (tools/lookup_micro.py via emc_bench_lookup,
+// variant 4): the plain gather lookup (macro_tcf) over (mat, E) pairs; the
+// staged production kernel is variant 8 (k_lookup_staged<1, ...>).
 __global__ void __launch_bounds__(256, 4) k_lookup_bench(int32_t n, DLib L, const double* __restrict__ Es,
                                                          const int32_t* __restrict__ mats, double* __restrict__ out)
 {
     EMC_WARP_LOOP(n) {
         int64_t i = emc_base_ + lane_id();
-        double E = i < n ? Es[i] : 1.0;
-        int32_t m = i < n ? mats[i] : 0;
-        if (VARIANT == 2) { E = __shfl_sync(kFull, E, 0); m = __shfl_sync(kFull, m, 0); }
-        if (i < n && VARIANT >= 4) {
+        if (i < n) {
             double st, sc, sf, snf;
-            double* ck = VARIANT == 6 ? nullptr : out + n + i;
-            if (VARIANT == 5) macro_tcf_simple(L, m, E, st, sc, sf, snf, ck, 16, n);
-            else if (VARIANT == 7) macro_tcf_pf(L, m, E, st, sc, sf, snf, ck, 16, n);
-            else macro_tcf(L, m, E, st, sc, sf, snf, ck, 16, n);
-            out[i] = st + sc + sf + snf;
-        } else if (i < n) {
-            const int32_t grp = __ldg(L.mat_group + m);
-            const int32_t e0 = __ldg(L.grp_off + grp), ncomp = __ldg(L.grp_off + grp + 1) - e0;
-            const int32_t bin = energy_bin(E, L);
-            const NucRef* __restrict__ refs = L.gnuc + e0;
-            const DD* __restrict__ dd = L.ddT + m;
-            double st = 0.0, sc = 0.0, sf = 0.0, snf = 0.0;
-            for (int32_t k = 0; k < ncomp; ++k) {
-                const NucRef r = refs[k];
-                const DD w = dd[(int64_t)k * L.n_mat];
-                double t, cc, f;
-                if (VARIANT == 3) {
-                    const double fr = __dmul_rn(E, 1e-9);
-                    t = lerp(1.0 + k, 2.0, fr); cc = lerp(0.5, 1.0 + k, fr); f = lerp(0.1, 0.3, fr);
-                } else {
-                    const int32_t h = __ldg(L.hash + r.hrow + bin);
-                    const Rec* __restrict__ R = L.rec + r.g0;
-                    const int32_t last = r.glen - 1;
-                    int32_t ii = h;
-                    Rec q0 = R[ii], q1 = R[ii + 1];
-                    while (q1.E <= E && ii + 1 < last) { ++ii; q0 = q1; q1 = R[ii + 1]; }
-                    if (ii == 0 && E <= q0.E) { t = q0.t; cc = q0.c; f = q0.f; }
-                    else if (E >= q1.E) { t = q1.t; cc = q1.c; f = q1.f; }
-                    else {
-                        const double fr = VARIANT == 1 ? __dmul_rn(__dsub_rn(E, q0.E), __dsub_rn(q1.E, q0.E))
-                                                       : frac(E, q0.E, q1.E);
-                        t = lerp(q0.t, q1.t, fr);
-                        cc = lerp(q0.c, q1.c, fr);
-                        f = lerp(q0.f, q1.f, fr);
-                    }
-                }
-                st = __dadd_rn(st, __dmul_rn(w.den, t));
-                sc = __dadd_rn(sc, __dmul_rn(w.den, cc));
-                sf = __dadd_rn(sf, __dmul_rn(w.den, f));
-                snf = __dadd_rn(snf, __dmul_rn(w.dn, f));
-            }
+            macro_tcf(L, mats[i], Es[i], st, sc, sf, snf, out + n + i, 16, n);
             out[i] = st + sc + sf + snf;
         }
     }
