@@ -312,6 +312,28 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                 bin[p] = energy_bin(E[p], L);
             }
         }
+        // particles of small groups (< LK_MIN_NUC nuclides: the moderator) are
+        // done right here, lane by lane, without the block-wide pass machinery
+        {
+            const bool ckon0 = MODE == 1 || fused;
+            const int64_t cks0 = MODE == 0 ? S.nslots : (int64_t)n;
+#pragma unroll
+            for (int p = 0; p < PPL; ++p) {
+                if (pend[p] && __ldg(L.grp_off + grp[p] + 1) - __ldg(L.grp_off + grp[p]) < LK_MIN_NUC) {
+                    double t0, c0, f0, n0;
+                    macro_tcf(L, m[p], E[p], t0, c0, f0, n0,
+                              ckon0 ? (MODE == 0 ? S.ckpt + s[p] : bout + n + i[p]) : nullptr, nck, cks0);
+                    if (MODE == 0) {
+                        P2 c; c.t = t0; c.c = c0; c.f = f0; c.nsf = n0;
+                        (rdst ? rdst : S.ps)[s[p]].c = c;
+                    } else {
+                        bout[i[p]] = t0 + c0 + f0 + n0;
+                    }
+                    nl += (unsigned long long)(__ldg(L.grp_off + grp[p] + 1) - __ldg(L.grp_off + grp[p]));
+                    pend[p] = false;
+                }
+            }
+        }
         // one pass per composition group present in the chunk (normally one)
         for (;;) {
             if (threadIdx.x == 0) { sh.grp = INT32_MAX; sh.bmin = INT32_MAX; sh.bmax = -1; }
