@@ -325,17 +325,24 @@ extern "C" int emc_upload_library(emc_ctx* c, const emc_library* lib)
             for (int32_t nid : sig)
                 hgnuc.push_back(NucRef{(int32_t)lib->grid_off[nid], (int32_t)(lib->grid_off[nid + 1] - lib->grid_off[nid]),
                                        (int32_t)(nid * nbins), nid});
+            // staged groups are padded to whole pipeline stages with copies of
+            // their first nuclide at zero density: den*t = +0 leaves every
+            // running sum bit-identical, and the consumers need no bound checks
+            if ((int32_t)sig.size() >= LK_MIN_NUC)
+                while ((hgnuc.size() - hgoff.back()) % LK_G) hgnuc.push_back(hgnuc[hgoff.back()]);
             hgoff.push_back((int32_t)hgnuc.size());
         }
         hgroup[m] = g;
     }
     if (hgnuc.empty()) hgnuc.push_back(NucRef{0, 1, 0, 0});
-    std::vector<DD> hdd((size_t)std::max(maxc, 1) * nm, DD{0.0, 0.0});
+    int32_t maxg = std::max(maxc, 1);          // longest (padded) group list
+    for (size_t g = 0; g + 1 < hgoff.size(); ++g) maxg = std::max(maxg, hgoff[g + 1] - hgoff[g]);
+    std::vector<DD> hdd((size_t)maxg * nm, DD{0.0, 0.0});
     for (int64_t m = 0; m < nm; ++m)
         for (int64_t k = lib->mat_off[m]; k < lib->mat_off[m + 1]; ++k)
             hdd[(size_t)(k - lib->mat_off[m]) * nm + m] = DD{hcomp[k].den, hcomp[k].dn};
     // staged lookup: densities as [stage][material][LK_G] blocks (one bulk copy per stage)
-    const int64_t nstage = (std::max(maxc, 1) + LK_G - 1) / LK_G;
+    const int64_t nstage = (maxg + LK_G - 1) / LK_G;
     std::vector<double> hden((size_t)nstage * nm * LK_DS, 0.0);
     for (int64_t m = 0; m < nm; ++m)
         for (int64_t k = lib->mat_off[m]; k < lib->mat_off[m + 1]; ++k) {

@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                     } else {
                         bout[i[p]] = t0 + c0 + f0 + n0;
                     }
-                    nl += (unsigned long long)(__ldg(L.grp_off + grp[p] + 1) - __ldg(L.grp_off + grp[p]));
+                    nl += (unsigned long long)(__ldg(L.mat_off + m[p] + 1) - __ldg(L.mat_off + m[p]));
                     pend[p] = false;
                 }
             }
@@ -428,10 +428,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                     const int d = (int)(T % LK_D);
                     mbar_wait(&sh.full[d], (T / LK_D) & 1);
                     if (any) {
+                        // staged group lists are whole stages (padded at upload)
 #pragma unroll
                         for (int j = 0; j < LK_G; ++j) {
                             const int k = t * LK_G + j;
-                            if (k >= ncomp) break;
                             const uint32_t wd = sh.word[d][j];
                             const IvRec* W = sh.iv[d][j];
                             // issued with the meta word (always in-bounds shared memory)
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                     } else {
                         bout[i[p]] = st[p] + sc[p] + sf[p] + snf[p];
                     }
-                    nl += (unsigned long long)ncomp;
+                    nl += (unsigned long long)(__ldg(L.mat_off + m[p] + 1) - __ldg(L.mat_off + m[p]));
                     pend[p] = false;
                 }
             }
