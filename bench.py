@@ -55,6 +55,14 @@ WORKLOAD_C5 = dict(workload="C5 shielding_slab(8 nuclides/material, 2000 points,
                    mesh=(100, 100, 120), seed=42)
 
 
+# --workload c1: BASELINE configs[0] (the reference's own CPU-runnable case, SURVEY 8 "C1")
+METRIC_C1 = "particles/s (active batches), UO2 pincell, 12 fuel nuclides (C1)"
+WORKLOAD_C1 = dict(workload="C1 pincell: depleted_pincell(12,3,100,8,seed=1), 10k particles/batch", ppb_per_gpu=10_000,
+                   mode="event", reduction="deterministic", seed=42)
+# --workload c3: BASELINE configs[2] (Hoogenboom-Martin small restated on the pincell, SURVEY 8 "C3")
+METRIC_C3 = "particles/s (active batches), HM-small fresh fuel (34 fuel nuclides)"
+WORKLOAD_C3 = dict(workload="C3 HM-small pincell: depleted_pincell(34,3,11303,100,seed=1)", ppb_per_gpu=10_000_000,
+                   mode="event", reduction="fast", seed=42)
 # --workload c2: BASELINE configs[1] (17x17 assembly, SURVEY 8f row 2 extension)
 METRIC_C2 = "particles/s (active batches), 2D 17x17 PWR assembly, ~30 nuclides"
 WORKLOAD_C2 = dict(workload="C2 pwr_assembly(27 fuel + 3 moderator nuclides, 11303 points, 17x17 lattice, "
@@ -68,6 +76,10 @@ def problem(args):
         return P.shielding_slab()
     if args.workload == "c2":
         return P.pwr_assembly()
+    if args.workload == "c3":
+        return P.depleted_pincell(34, 3, 11303, 100, seed=1)
+    if args.workload == "c1":
+        return P.depleted_pincell(12, 3, 100, 8, seed=1)
     return P.depleted_pincell(272, 3, 11303, 100, seed=1)
 BYTES_PER_NUCLIDE_LOOKUP = 64
 TRAFFIC_PROFILE = "r1s4_lookup_traffic.json"
@@ -83,7 +95,8 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle sampling during the timed region."""
+    """Clocks/throttle sampling during the timed region: NVML in-process (the
+    library behind nvidia-smi), else `nvidia-smi --query-gpu` (BENCH_CLOCKS=smi)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -95,7 +108,34 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _run_nvml(self):
+        # the library nvidia-smi reads: same fields without spawning a process
+        # (and re-initialising NVML) every sample, which stalls short batches
+        import pynvml as nv
+        nv.nvmlInit()
+        try:
+            h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            bits = (0x8, 0x40, 0x20, 0x4)      # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+            while not self._stop.is_set():
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except AttributeError:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.rows.append([str(self.gpu), str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                  str(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)),
+                                  str(nv.nvmlDeviceGetPowerUsage(h) / 1000.0), hex(r)]
+                                 + ["Active" if r & b else "Not Active" for b in bits])
+                self._stop.wait(0.2)
+        finally:
+            nv.nvmlShutdown()
+
     def _run(self):
+        if os.environ.get("BENCH_CLOCKS", "nvml") == "nvml":
+            try:
+                self._run_nvml()
+                return
+            except Exception:  # noqa: BLE001
+                self.rows = []
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), "--format=csv,noheader,nounits",
@@ -182,13 +222,13 @@ def run_reference(args):
                sort_enabled=True, sort_every_n=1, seed=42, workers=threads, **ext)
     res = driver.run(cfg, lib.arrays(), cell.as_tuple(), workers=threads)
     v = res["active_rate"]
-    line = {"impl": "reference", "metric": {"c2": METRIC_C2, "c5": METRIC_C5}.get(args.workload, METRIC),
+    line = {"impl": "reference", "metric": {"c1": METRIC_C1, "c2": METRIC_C2, "c3": METRIC_C3, "c5": METRIC_C5}.get(args.workload, METRIC),
             "value": v, "unit": "particles/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * res["active_wall"] / max(args.steps, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": dict({"c2": WORKLOAD_C2, "c5": WORKLOAD_C5}.get(args.workload, WORKLOAD),
+            "config": dict({"c1": WORKLOAD_C1, "c2": WORKLOAD_C2, "c3": WORKLOAD_C3, "c5": WORKLOAD_C5}.get(args.workload, WORKLOAD),
                            reduction="deterministic (reference default)",
                            ppb_sample=ppb,
                            impl="C restatement of the reference kernels (oracle/, bit-exact with the "
@@ -211,13 +251,13 @@ def run_ours(args):
     lib, cell = problem(args)
     t_lib = time.perf_counter() - t0
     c5 = args.workload == "c5"
-    wl = {"c2": WORKLOAD_C2, "c5": WORKLOAD_C5}.get(args.workload, WORKLOAD)
+    wl = {"c1": WORKLOAD_C1, "c2": WORKLOAD_C2, "c3": WORKLOAD_C3, "c5": WORKLOAD_C5}.get(args.workload, WORKLOAD)
     ppb_gpu = args.particles or wl["ppb_per_gpu"]
     ext = dict(run_mode="fixed_source", mesh=WORKLOAD_C5["mesh"]) if c5 else {}
     cfg = P.RunConfig(particles_per_batch=ppb_gpu * ws, inactive_batches=args.warmup,
                       active_batches=args.steps, mode="event", sort_enabled=True,
                       max_in_flight=args.max_in_flight or ppb_gpu, tally_mode="fused",
-                      reduction="fast", seed=42, workers=ws, **ext)
+                      reduction=wl["reduction"], seed=42, workers=ws, **ext)
     dev = torch.cuda.current_device()
     eng = replication.engine_for(dev, lib, cell)
     stream = torch.cuda.current_stream()
@@ -268,7 +308,7 @@ def run_ours(args):
     except Exception:  # noqa: BLE001
         traffic = None
     line = {
-        "metric": {"c2": METRIC_C2, "c5": METRIC_C5}.get(args.workload, METRIC), "value": value,
+        "metric": {"c1": METRIC_C1, "c2": METRIC_C2, "c3": METRIC_C3, "c5": METRIC_C5}.get(args.workload, METRIC), "value": value,
         "unit": "particles/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -311,9 +351,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--particles", type=int, default=0,
                     help="particles per GPU per batch (default 40M for c4, 10M for c5)")
-    ap.add_argument("--workload", default="c4", choices=("c4", "c2", "c5"),
+    ap.add_argument("--workload", default="c4", choices=("c4", "c1", "c2", "c3", "c5"),
                     help="c4: headline HM-large eigenvalue (BASELINE metric); c2: 17x17 assembly; "
-                         "c5: fixed-source slab + mesh")
+                         "c3: HM-small; c5: fixed-source slab + mesh")
     ap.add_argument("--max-in-flight", type=int, default=0)
     ap.add_argument("--cpu-particles", type=int, default=0)
     ap.add_argument("--ref-particles", type=int, default=0)

@@ -63,10 +63,26 @@ __global__ void k_log_fold(const uint64_t* __restrict__ keys, const double* __re
 {
     int32_t b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= n_bins) return;
-    int64_t lo = 0, hi = n;                       // first key with bin >= b
-    while (lo < hi) { int64_t mid = (lo + hi) >> 1; if ((int64_t)(keys[mid] >> shift) < b) lo = mid + 1; else hi = mid; }
+    // [first key with bin >= b, first key with bin >= b + 1): the left fold over
+    // the range then has no load-dependent exit, so value loads run ahead of the
+    // (inherently serial, order-defining) add chain
+    int64_t r[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        int64_t lo = 0, hi = n;
+        while (lo < hi) { int64_t mid = (lo + hi) >> 1; if ((int64_t)(keys[mid] >> shift) < b + k) lo = mid + 1; else hi = mid; }
+        r[k] = lo;
+    }
     double s = init[b];
-    for (int64_t e = lo; e < n && (int64_t)(keys[e] >> shift) == b; ++e) s = __dadd_rn(s, vals[e]);
+    int64_t e = r[0];
+    for (; e + 8 <= r[1]; e += 8) {
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __ldg(vals + e + j);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) s = __dadd_rn(s, v[j]);
+    }
+    for (; e < r[1]; ++e) s = __dadd_rn(s, vals[e]);
     out[b] = s;
 }
 
