@@ -147,6 +147,7 @@ struct emc_ctx {
     bool staged = true;          // k_lookup_staged + energy-major sort (EMC_LOOKUP=plain: k_lookup)
     size_t lk_smem = 0;
     int lk_cfg = 0;              // staged-lookup launch configuration (EMC_LK_CFG)
+    bool lk_piped = true;        // chunk-pipelined staged lookup on sorted queues (EMC_LK_PIPED)
     DSlots S{};
 
     // queues + sort scratch
@@ -397,7 +398,7 @@ extern "C" int emc_upload_library(emc_ctx* c, const emc_library* lib)
     c->L = DLib{c->rec.p, c->ch_s.p, c->nu.p, c->mat_off.p, c->comp.p, c->hash.p, key_lo, (int32_t)nbins,
                 shift, lo, hi, c->mat_group.p, c->grp_off.p, c->gnuc.p, c->ddT.p, (int32_t)nm, 0,
                 c->iv.p, c->denS.p, den_staged, 0, c->nsafe.p};
-    c->lk_smem = lk_smem_bytes((int)nm, den_staged);
+    c->lk_smem = lk_pipe_offset((int)nm, den_staged) + sizeof(LkPipe);
     EMC_TRY_CUDA(lk_set_smem(c->lk_smem));
     if (const char* lc = getenv("EMC_LK_CFG")) c->lk_cfg = std::max(0, std::min(LK_NCFG - 1, atoi(lc)));
     c->n_materials = (int32_t)nm;
@@ -525,6 +526,8 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
     rc |= c->ps.alloc(nslots);
     if (const char* lb = getenv("EMC_LOOKUP_BLOCK")) c->lookup_block = atoi(lb);
     if (const char* lk = getenv("EMC_LOOKUP")) c->staged = std::strcmp(lk, "plain") != 0;
+    c->lk_piped = true;
+    if (const char* lp = getenv("EMC_LK_PIPED")) c->lk_piped = atoi(lp) != 0;
     const char* ro = getenv("EMC_REORDER");
     c->reorder = !(ro && ro[0] == '0');
     if (c->reorder) rc |= c->ps2.alloc(nslots);
@@ -654,6 +657,18 @@ static int sort_cub64(emc_ctx* c, const K* kin, K* kout, const V* vin, V* vout, 
                                                  c->stream));
     c->launches += (end_bit + 7) / 8;
     return 0;
+}
+
+// layout of the staged path's sort key (lookup_key): group | ebin | material | fine energy bits
+static LkKeys lk_keys(const emc_ctx* c, const uint32_t* keys)
+{
+    LkKeys K;
+    K.keys = keys;
+    K.eb_shift = c->mat_bits + c->band_bits;
+    K.grp_shift = c->ebin_bits + K.eb_shift;
+    K.eb_mask = c->ebin_bits ? (uint32_t)((1ull << c->ebin_bits) - 1) : 0u;
+    K.ebin_shift = c->ebin_shift;
+    return K;
 }
 
 static int bits_for(int64_t v)
@@ -810,8 +825,12 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
                 // the staged lookup moves the lines into sorted order itself (fused reorder)
                 PState* rdst = nullptr;
                 if (do_sort && c->reorder) rdst = c->ps_cur == c->ps.p ? c->ps2.p : c->ps.p;
-                EMC_TRY_CUDA(lk_launch<0>(c->lk_cfg, c->L, q, nL, c->S, cf.fused, c->cnt.p, nullptr, nullptr, nullptr,
-                                          c->sm_count, c->lk_smem, st, nullptr, rdst));
+                if (do_sort && c->lk_piped)
+                    EMC_TRY_CUDA(lk_launch_piped<0>(c->L, q, nL, c->S, cf.fused, c->cnt.p, nullptr, nullptr, nullptr,
+                                                    c->sm_count, c->lk_smem, st, rdst, lk_keys(c, c->keys_out.p)));
+                else
+                    EMC_TRY_CUDA(lk_launch<0>(c->lk_cfg, c->L, q, nL, c->S, cf.fused, c->cnt.p, nullptr, nullptr,
+                                              nullptr, c->sm_count, c->lk_smem, st, nullptr, rdst));
                 if (rdst) {
                     c->ps_cur = rdst;
                     c->S.ps = rdst;
@@ -1285,6 +1304,23 @@ extern "C" int emc_div_eval(emc_ctx* c, int64_t n, const double* num, const doub
     return 0;
 }
 
+// lookup microbenchmark: the staged path's sort key of each (E, mat) pair
+namespace emc {
+__global__ void k_bench_keys(int32_t n, DLib L, const double* __restrict__ E, const int32_t* __restrict__ M, QKeys K,
+                             int32_t* __restrict__ idx)
+{
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) { K.keys[i] = lookup_key(L, K, E[i], M[i]); idx[i] = i; }
+}
+
+__global__ void k_bench_permute(int32_t n, const int32_t* __restrict__ perm, const double* __restrict__ E,
+                                const int32_t* __restrict__ M, double* __restrict__ Eo, int32_t* __restrict__ Mo)
+{
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) { Eo[i] = E[perm[i]]; Mo[i] = M[perm[i]]; }
+}
+}  // namespace emc
+
 // test/tuning entry point: time k_lookup_bench<variant> over n (mat, E) pairs
 extern "C" int emc_bench_lookup(emc_ctx* c, int64_t n, const int32_t* mats, const double* E, int32_t variant,
                                 int32_t iters, double* ms_out, double* checksum)
@@ -1295,12 +1331,31 @@ extern "C" int emc_bench_lookup(emc_ctx* c, int64_t n, const int32_t* mats, cons
     DBuf<int32_t> dm; DBuf<double> de, dout;
     if (to_dev(dm, mats, n, st) || to_dev(de, E, n, st) || dout.alloc(n * 17)) return EMC_E_OOM;
     int grid = c->sm_count * 16;
+    DBuf<uint32_t> dk;          // variant 9: pairs put in sort-key order, keys kept for the kernel
+    if (variant == 9) {
+        if (!c->staged || !c->configured) return fail_arg("emc_bench_lookup: variant 9 needs a configured staged library");
+        DBuf<uint32_t> k0; DBuf<int32_t> i0, i1, m1; DBuf<double> e1;
+        if (dk.alloc(n) || k0.alloc(n) || i0.alloc(n) || i1.alloc(n) || m1.alloc(n) || e1.alloc(n)) return EMC_E_OOM;
+        k_bench_keys<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p,
+            QKeys{k0.p, c->ebin_bits, c->ebin_shift, c->mat_bits, c->band_bits}, i0.p);
+        EMC_CHECK_LAUNCH(c);
+        if (int rc = sort_cub(c, k0.p, dk.p, i0.p, i1.p, (int)n, c->key_bits)) return rc;
+        k_bench_permute<<<grid_for(n, 256, 1 << 30), 256, 0, st>>>((int32_t)n, i1.p, de.p, dm.p, e1.p, m1.p);
+        EMC_CHECK_LAUNCH(c);
+        EMC_TRY_CUDA(cudaMemcpyAsync(de.p, e1.p, n * 8, cudaMemcpyDeviceToDevice, st));
+        EMC_TRY_CUDA(cudaMemcpyAsync(dm.p, m1.p, n * 4, cudaMemcpyDeviceToDevice, st));
+        EMC_TRY_CUDA(cudaStreamSynchronize(st));
+        k0.release(); i0.release(); i1.release(); m1.release(); e1.release();
+    }
     float total = 0;
     for (int it = 0; it <= iters; ++it) {
         EMC_TRY_CUDA(cudaEventRecord(c->ev[0], st));
         if (variant == 8) {
             EMC_TRY_CUDA(lk_launch<1>(c->lk_cfg, c->L, nullptr, n, c->S, 1, c->cnt.p, de.p, dm.p, dout.p, c->sm_count,
                                       c->lk_smem, st));
+        } else if (variant == 9) {
+            EMC_TRY_CUDA(lk_launch_piped<1>(c->L, nullptr, n, c->S, 1, c->cnt.p, de.p, dm.p, dout.p, c->sm_count,
+                                            c->lk_smem, st, nullptr, lk_keys(c, dk.p)));
         } else {
             k_lookup_bench<<<grid, 256, 0, st>>>((int32_t)n, c->L, de.p, dm.p, dout.p);
         }
@@ -1318,6 +1373,6 @@ extern "C" int emc_bench_lookup(emc_ctx* c, int64_t n, const int32_t* mats, cons
     double cs = 0;
     for (double v : h) cs += v;
     *checksum = cs;
-    dm.release(); de.release(); dout.release();
+    dm.release(); de.release(); dout.release(); dk.release();
     return 0;
 }

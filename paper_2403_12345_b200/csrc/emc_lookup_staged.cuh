@@ -104,9 +104,21 @@ __device__ __forceinline__ bool mbar_try_wait(unsigned long long* b, uint32_t pa
     return ok != 0;
 }
 
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity)
+// a wait that cannot complete is a bug: report it and trap instead of hanging
+// the device (try_wait suspends for a while per call, so ~2^26 calls is far
+// beyond any legitimate wait)
+__device__ __noinline__ void mbar_stuck(const unsigned long long* b, uint32_t parity, uint32_t tag)
 {
+    printf("emc: mbarrier wait stuck: block %d thread %d smem 0x%x parity %u tag 0x%x\n", (int)blockIdx.x,
+           (int)threadIdx.x, smem_addr(b), parity, tag);
+    __trap();
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity, uint32_t tag = 0)
+{
+    uint32_t spins = 0;
     while (!mbar_try_wait(b, parity)) {
+        if (++spins == (1u << 26)) mbar_stuck(b, parity, tag);
     }
 }
 
@@ -202,9 +214,11 @@ __device__ __forceinline__ void lk_micro_slow(const DLib& L, const LkMeta& mt, u
     if (cnt_ <= 4) {
         li = min((int32_t)(a1 <= E) + (int32_t)(a2 <= E), cnt_ - 2);
     } else {
-        const int32_t lim = mt.last - mt.lo;
-        li = __ldg(L.hash + mt.hrow + bin) - mt.lo;
-        while (li + 1 < lim && W[li + 1].E0 <= E) ++li;
+        // the reference's scan (hash bound, then forward while grid[i+1] <= E)
+        // ends at the last record <= E of the ascending grid: count them in the
+        // staged window (warp-uniform trip count, broadcast shared loads)
+        li = 0;
+        for (int32_t j = 1; j <= cnt_ - 2; ++j) li += (int32_t)pos_le(W[j].E0, E);
     }
     const double e0v = W[li].E0, e1 = W[li + 1].E0;
     const bool lo_clamp = mt.lo + li == 0 && E <= e0v, hi_clamp = e1 <= E;
@@ -508,6 +522,273 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Chunk-pipelined variant (sorted queues).  The producer warp plans chunk c's
+// passes (composition groups and energy-bin ranges) from the SORTED push-time
+// keys instead of waiting for the consumers to load their particles and
+// reduce over the block, publishes the plan in a two-slot descriptor ring
+// (mbarriers, no __syncthreads in the chunk loop) and streams chunk c+1's
+// first stages while the consumers are still folding chunk c.  Consumers check
+// their own (group, bin) against the plan; a particle no pass covers (small
+// groups, more than LK_MAXP groups in a chunk, or keys that do not match the
+// particle) takes the per-lane global path, so correctness never depends on
+// the keys -- only the speed does.
+constexpr int LK_MAXP = 4;
+
+struct LkKeys {
+    const uint32_t* keys;          // sorted keys, aligned with the queue
+    int32_t grp_shift;             // key >> grp_shift = composition group
+    int32_t eb_shift;              // (key >> eb_shift) & eb_mask = energy bin >> ebin_shift
+    uint32_t eb_mask;
+    int32_t ebin_shift;
+};
+
+struct __align__(16) LkPipe {
+    unsigned long long dfull[2], dempty[2];
+    int32_t npass[2];
+    int32_t G[2][LK_MAXP], bmin[2][LK_MAXP], bmax[2][LK_MAXP];
+};
+
+__host__ __device__ constexpr size_t lk_pipe_offset(int n_mat, int den_staged)
+{
+    return (lk_smem_bytes(n_mat, den_staged) + 15) & ~(size_t)15;
+}
+
+template <int MODE, bool DEN_ST>
+__global__ void __launch_bounds__(1024, 1)
+    k_lookup_piped(const int32_t* __restrict__ q, int32_t n, DLib L, DSlots S, int32_t fused,
+                   unsigned long long* cnt, const double* __restrict__ bE, const int32_t* __restrict__ bM,
+                   double* __restrict__ bout, PState* __restrict__ rdst, LkKeys K)
+{
+    constexpr int NW = 32, LK_CONS = NW - 1, LK_CHUNK = LK_CONS * 32;
+    extern __shared__ __align__(128) unsigned char lk_raw[];
+    LkShared& sh = *reinterpret_cast<LkShared*>(lk_raw);
+    double* const sden = reinterpret_cast<double*>(lk_raw + sizeof(LkShared));
+    const int32_t nmat = L.n_mat;
+    LkPipe& P = *reinterpret_cast<LkPipe*>(lk_raw + lk_pipe_offset(nmat, DEN_ST));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool producer = warp == LK_CONS;
+    const int32_t nck = MODE == 0 ? S.nck : 16;
+    const bool ckon = MODE == 1 || fused;
+    const int64_t cks = MODE == 0 ? S.nslots : (int64_t)n;
+
+    if (threadIdx.x == 0) {
+        for (int d = 0; d < LK_D; ++d) {
+            mbar_init(&sh.full[d], 32);
+            mbar_init(&sh.empty[d], LK_CONS);
+        }
+        for (int k = 0; k < 2; ++k) {
+            mbar_init(&P.dfull[k], 1);
+            mbar_init(&P.dempty[k], LK_CONS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    uint32_t T = 0;                 // pipeline stage counter (same sequence in every warp)
+    uint32_t c = 0;                 // chunk counter of this CTA
+    unsigned long long nl = 0;
+    for (int64_t base = (int64_t)blockIdx.x * LK_CHUNK; base < n; base += (int64_t)gridDim.x * LK_CHUNK, ++c) {
+        const int slot = (int)(c & 1u);
+        const uint32_t use = c >> 1;
+        if (producer) {
+            // ---- plan: group runs of the sorted chunk -> passes
+            if (c >= 2) mbar_wait(&P.dempty[slot], (use - 1) & 1, 0x40000u | c);
+            const int64_t end = min(base + (int64_t)LK_CHUNK, (int64_t)n);
+            int np = 0;
+            int64_t s0 = base;
+            while (s0 < end && np < LK_MAXP) {
+                const uint32_t ka = __ldg(K.keys + s0);
+                const uint32_t g = ka >> K.grp_shift;
+                int64_t e = end;
+                if ((__ldg(K.keys + end - 1) >> K.grp_shift) != g) {
+                    for (int64_t j0 = s0 + 1; j0 < end; j0 += 32) {
+                        const int64_t j = j0 + lane;
+                        const bool brk = j < end && (__ldg(K.keys + j) >> K.grp_shift) != g;
+                        const unsigned bal = __ballot_sync(0xffffffffu, brk);
+                        if (bal) { e = j0 + __ffs(bal) - 1; break; }
+                    }
+                }
+                const uint32_t kb = __ldg(K.keys + e - 1);
+                const int32_t ncomp = __ldg(L.grp_off + g + 1) - __ldg(L.grp_off + g);
+                if (ncomp >= LK_MIN_NUC) {
+                    const int32_t lo = (int32_t)(((ka >> K.eb_shift) & K.eb_mask) << K.ebin_shift);
+                    const int32_t hi = min((int32_t)(((((kb >> K.eb_shift) & K.eb_mask) + 1) << K.ebin_shift) - 1),
+                                           L.nbins - 1);
+                    if (lane == 0) { P.G[slot][np] = (int32_t)g; P.bmin[slot][np] = lo; P.bmax[slot][np] = hi; }
+                    ++np;
+                }
+                s0 = e;
+            }
+            if (lane == 0) {
+                P.npass[slot] = np;
+                mbar_arrive(&P.dfull[slot]);     // release: the plan is visible to the waiting consumers
+            }
+            __syncwarp();
+            // ---- stream the passes' stages (lane j < LK_G owns nuclide 8t+j)
+            for (int p = 0; p < np; ++p) {
+                const int32_t G = P.G[slot][p], bmin = P.bmin[slot][p], bmax = P.bmax[slot][p];
+                const int32_t e0 = __ldg(L.grp_off + G), ncomp = __ldg(L.grp_off + G + 1) - e0;
+                const int nst = (ncomp + LK_G - 1) / LK_G;
+                LkNext nx;
+                nx.valid = false;
+                if (lane < LK_G) lk_prefetch(L, e0, lane, ncomp, bmin, bmax, nx);
+                for (int t = 0; t < nst; ++t, ++T) {
+                    const int d = (int)(T % LK_D);
+                    const LkNext cur = nx;
+                    if (lane < LK_G && t + 1 < nst) lk_prefetch(L, e0, (t + 1) * LK_G + lane, ncomp, bmin, bmax, nx);
+                    if (T >= (uint32_t)LK_D) mbar_wait(&sh.empty[d], ((T / LK_D) - 1) & 1, 0x10000u | T);
+                    uint32_t bytes = 0;
+                    const bool copy_iv = lane < LK_G && cur.valid && cur.mt.mode != LK_GLOBAL;
+                    if (lane < LK_G && cur.valid) {
+                        sh.meta[d][lane] = cur.mt;
+                        sh.word[d][lane] = lk_word(cur.mt.cnt, cur.mt.mode, cur.mt.lo, cur.mt.last);
+                    }
+                    if (copy_iv) bytes += (uint32_t)cur.mt.cnt * (uint32_t)sizeof(IvRec);
+                    if (DEN_ST && lane == 0) bytes += (uint32_t)lk_den_block(nmat);
+                    mbar_arrive_tx(&sh.full[d], bytes);
+                    if (copy_iv)
+                        bulk_g2s(&sh.iv[d][lane][0], L.iv + cur.mt.g0 + cur.mt.lo,
+                                 (uint32_t)cur.mt.cnt * (uint32_t)sizeof(IvRec), &sh.full[d]);
+                    if (DEN_ST && lane == 0)
+                        bulk_g2s(sden + (size_t)d * nmat * LK_DS, L.denS + (size_t)t * nmat * LK_DS,
+                                 (uint32_t)lk_den_block(nmat), &sh.full[d]);
+                }
+            }
+            continue;
+        }
+
+        // ---- consumers: load the particle (fused reorder) while the plan is made
+        const int64_t i = base + (int64_t)threadIdx.x;
+        bool pend = i < n;
+        int32_t s = 0, m = 0, grp = -1, bin = 0;
+        double E = 1.0;
+        if (pend) {
+            if (MODE == 0 && rdst) {
+                const PState line = S.ps[q[i]];
+                rdst[i] = line;
+                s = (int32_t)i;
+                E = line.a.E;
+                m = line.d.mat;
+            } else if (MODE == 0) {
+                s = q[i];
+                E = S.ps[s].a.E;
+                m = S.ps[s].d.mat;
+            } else {
+                E = bE[i];
+                m = bM[i];
+            }
+            grp = __ldg(L.mat_group + m);
+            bin = energy_bin(E, L);
+        }
+        mbar_wait(&P.dfull[slot], use & 1, 0x30000u | c);
+        const int np = P.npass[slot];
+        int pidx = -1;
+        for (int p = 0; p < np; ++p)
+            if (pidx < 0 && grp == P.G[slot][p] && bin >= P.bmin[slot][p] && bin <= P.bmax[slot][p]) pidx = p;
+        if (pend && pidx < 0) {
+            // not covered by a pass: small group (the moderator) or an odd chunk
+            double t0, c0, f0, n0;
+            macro_tcf(L, m, E, t0, c0, f0, n0, ckon ? (MODE == 0 ? S.ckpt + s : bout + n + i) : nullptr, nck, cks);
+            if (MODE == 0) {
+                P2 cc; cc.t = t0; cc.c = c0; cc.f = f0; cc.nsf = n0;
+                (rdst ? rdst : S.ps)[s].c = cc;
+            } else {
+                bout[i] = t0 + c0 + f0 + n0;
+            }
+            nl += (unsigned long long)(__ldg(L.mat_off + m + 1) - __ldg(L.mat_off + m));
+            pend = false;
+        }
+        for (int p = 0; p < np; ++p) {
+            const int32_t G = P.G[slot][p];
+            const int32_t ncomp = __ldg(L.grp_off + G + 1) - __ldg(L.grp_off + G);
+            const int nst = (ncomp + LK_G - 1) / LK_G;
+            const bool mine = pend && pidx == p;
+            const bool any = __any_sync(0xffffffffu, mine);
+            // lanes outside the pass compute on a member's copy (results discarded)
+            const int src_lane = any ? __ffs(__ballot_sync(0xffffffffu, mine)) - 1 : 0;
+            // (the shuffles are executed by every lane: a full-mask shuffle under
+            // a lane-dependent condition is undefined)
+            const double Es = __shfl_sync(0xffffffffu, E, src_lane);
+            const int32_t bs = __shfl_sync(0xffffffffu, bin, src_lane);
+            const int32_t ms = __shfl_sync(0xffffffffu, m, src_lane);
+            const double Eu = mine ? E : Es;
+            const int32_t bu = mine ? bin : bs;
+            const int32_t mu = mine ? m : ms;
+            double st = 0.0, sc = 0.0, sf = 0.0, snf = 0.0;
+            for (int t = 0; t < nst; ++t, ++T) {
+                const int d = (int)(T % LK_D);
+                mbar_wait(&sh.full[d], (T / LK_D) & 1, 0x20000u | T);
+                if (any) {
+#pragma unroll
+                    for (int j = 0; j < LK_G; ++j) {
+                        const int k = t * LK_G + j;
+                        const uint32_t wd = sh.word[d][j];
+                        const IvRec* W = sh.iv[d][j];
+                        const double a1 = W[1].E0, a2 = W[2].E0;
+                        double tt, cc, ff;
+                        if (__builtin_expect(wd <= 4u, 1)) {
+                            const int32_t li = min((int32_t)(a1 <= Eu) + (int32_t)(a2 <= Eu), (int32_t)wd - 2);
+                            const double2 er = *reinterpret_cast<const double2*>(&W[li].E0);
+                            const double e1 = W[li + 1].E0;
+                            const IvRec& a = W[li];
+                            const double fr = div_by_rcp_safe(__dsub_rn(Eu, er.x), __dsub_rn(e1, er.x), er.y);
+                            tt = __dadd_rn(a.t0, __dmul_rn(fr, a.dt));
+                            cc = __dadd_rn(a.c0, __dmul_rn(fr, a.dc));
+                            ff = __dadd_rn(a.f0, __dmul_rn(fr, a.df));
+                        } else {
+                            lk_micro_slow(L, sh.meta[d][j], wd, W, a1, a2, bu, Eu, tt, cc, ff);
+                        }
+                        const double2 dd =
+                            DEN_ST ? *reinterpret_cast<const double2*>(sden + ((size_t)d * nmat + mu) * LK_DS + 2 * j)
+                                   : *reinterpret_cast<const double2*>(&L.ddT[(int64_t)k * nmat + mu]);
+                        st = __dadd_rn(st, __dmul_rn(dd.x, tt));
+                        sc = __dadd_rn(sc, __dmul_rn(dd.x, cc));
+                        sf = __dadd_rn(sf, __dmul_rn(dd.x, ff));
+                        snf = __dadd_rn(snf, __dmul_rn(dd.y, ff));
+                    }
+                    if (ckon && (t & 1) && (t + 1) * LK_G <= ncomp) {
+                        const int32_t row = t >> 1;
+                        double* ckb = MODE == 0 ? S.ckpt + s : bout + n + i;
+                        if (mine && row < nck) ckb[(int64_t)row * cks] = st;
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sh.empty[d]);
+            }
+            if (mine) {
+                if (MODE == 0) {
+                    P2 cc; cc.t = st; cc.c = sc; cc.f = sf; cc.nsf = snf;
+                    (rdst ? rdst : S.ps)[s].c = cc;
+                } else {
+                    bout[i] = st + sc + sf + snf;
+                }
+                nl += (unsigned long long)(__ldg(L.mat_off + m + 1) - __ldg(L.mat_off + m));
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&P.dempty[slot]);
+    }
+    if (MODE == 0 && !producer) {
+        warp_add_u64(cnt + CNT_INTERP_TRANSPORT, 4ull * nl);
+        warp_add_u64(cnt + CNT_NUCLIDE_LOOKUPS, nl);
+    }
+}
+
+template <int MODE>
+inline cudaError_t lk_launch_piped(const DLib& L, const int32_t* q, int64_t n, DSlots S, int32_t fused,
+                                   unsigned long long* cnt, const double* bE, const int32_t* bM, double* bout,
+                                   int sm_count, size_t smem, cudaStream_t st, PState* rdst, const LkKeys& K)
+{
+    constexpr int64_t chunk = 31 * 32;
+    const unsigned nb = (unsigned)std::min<int64_t>((n + chunk - 1) / chunk, (int64_t)sm_count);
+    if (L.den_staged)
+        k_lookup_piped<MODE, true><<<nb, 1024, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM, bout, rdst, K);
+    else
+        k_lookup_piped<MODE, false><<<nb, 1024, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM, bout, rdst, K);
+    return cudaGetLastError();
+}
+
 }  // namespace emc
 
 namespace emc {
@@ -569,6 +850,12 @@ inline cudaError_t lk_set_smem(size_t smem)
     if ((e = lk_set_smem_cfg<0, 0>(smem)) || (e = lk_set_smem_cfg<0, 1>(smem)) || (e = lk_set_smem_cfg<0, 2>(smem)) ||
         (e = lk_set_smem_cfg<0, 3>(smem)) || (e = lk_set_smem_cfg<1, 0>(smem)) || (e = lk_set_smem_cfg<1, 1>(smem)) ||
         (e = lk_set_smem_cfg<1, 2>(smem)) || (e = lk_set_smem_cfg<1, 3>(smem)))
+        return e;
+    const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    if ((e = cudaFuncSetAttribute(k_lookup_piped<0, true>, a, (int)smem)) ||
+        (e = cudaFuncSetAttribute(k_lookup_piped<0, false>, a, (int)smem)) ||
+        (e = cudaFuncSetAttribute(k_lookup_piped<1, true>, a, (int)smem)) ||
+        (e = cudaFuncSetAttribute(k_lookup_piped<1, false>, a, (int)smem)))
         return e;
     return cudaSuccess;
 }

@@ -230,6 +230,35 @@ def test_staged_lookup_equals_plain_c4(ppb):
     assert a.counters["interp_transport"] == b.counters["interp_transport"]
 
 
+@pytest.mark.parametrize("problem", ["c3", "c2"])
+def test_piped_lookup_equals_chunk_synchronous(problem):
+    """The chunk-pipelined staged lookup (plan from the sorted keys, production)
+    against the chunk-synchronous staged kernel (plan reduced over the block):
+    identical histories, k series, banks and counters, on libraries whose
+    chunks mix composition groups (C2: 2-D assembly) and carry small groups."""
+    if problem == "c3":
+        lib, cell = P.depleted_pincell(34, 3, 11303, 100, seed=1)
+    else:
+        lib, cell = P.pwr_assembly()
+    cfg = P.RunConfig(particles_per_batch=300_000, inactive_batches=1, active_batches=2, mode="event",
+                      seed=7, max_in_flight=300_000, reduction="deterministic")
+    old = os.environ.get("EMC_LK_PIPED")
+    try:
+        os.environ["EMC_LK_PIPED"] = "1"
+        a = P.run_replicated(cfg, lib, cell)
+        os.environ["EMC_LK_PIPED"] = "0"
+        b = P.run_replicated(cfg, lib, cell)
+    finally:
+        if old is None:
+            os.environ.pop("EMC_LK_PIPED", None)
+        else:
+            os.environ["EMC_LK_PIPED"] = old
+    assert np.array_equal(a.keff.values, b.keff.values)
+    assert np.array_equal(a.batch_sums, b.batch_sums)
+    assert a.physics_fingerprint() == b.physics_fingerprint()
+    assert a.counters == b.counters
+
+
 def test_staged_division_is_ieee():
     """The staged lookup divides by a precomputed reciprocal plus one FMA
     correction; it must equal the IEEE division bit for bit on every grid

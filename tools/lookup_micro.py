@@ -21,6 +21,9 @@ variants = [int(v) for v in sys.argv[2:]] or [0, 1, 2, 3]
 lib, cell = P.depleted_pincell(272, 3, 11303, 100, seed=1)
 eng = DeviceEngine(0)
 eng.upload_library(lib)
+if 9 in variants:      # the pipelined kernel needs the configured sort-key layout
+    eng.upload_geometry(cell)
+    eng.configure(P.RunConfig(particles_per_batch=1000, max_in_flight=1000), 0, 1000)
 rng = np.random.default_rng(1)
 mats = np.where(rng.random(n) < 0.7, rng.integers(0, 100, n), 100).astype(np.int32)
 E = -1.3e6 * np.log(1 - rng.random(n))
@@ -28,14 +31,15 @@ k = rng.poisson(2.6, n)
 for j in range(k.max()):
     E = np.where(k > j, E * (0.5 + 0.5 * rng.random(n)), E)
 E = np.clip(E, 1e-5, 2e7)
-# material-major (plain kernels) and (group, E, material) order (staged kernel, variant 8)
+# material-major (plain kernels) and (group, E, material) order (staged kernels:
+# 8 = k_lookup_staged, 9 = k_lookup_piped on the production sort key)
 order_m = np.lexsort((E, mats))
 ebin = np.floor(np.log2(E) * 512).astype(np.int64)     # ~ the production sort's log-hash bin
 order_e = np.lexsort((mats, ebin, mats == 100))
 ncomp = np.where(mats < 100, 272, 3)
 nl = int(ncomp.sum())
 for v in variants:
-    o = order_e if v == 8 else order_m
+    o = order_e if v in (8, 9) else order_m     # variant 9 re-sorts by the production key
     mo, Eo = np.ascontiguousarray(mats[o]), np.ascontiguousarray(E[o])
     ms, cs = C.c_double(), C.c_double()
     N.check(eng.lib.emc_bench_lookup(eng._h, n, N.ptr(mo), N.ptr(Eo), v, 5, C.byref(ms), C.byref(cs)), "bench")
