@@ -19,7 +19,7 @@ e2e       = RunResult.active_rate of the same run_event() call: the
             reference's own metric definition (replication.py:282-304, host
             wall per batch incl. host merge/reduce/resample and the per-batch
             D2H of counters/tallies), i.e. through the public API.
-roofline  = XS-lookup kernel (k_lookup_staged): algorithmic bytes = 64 B per
+roofline  = XS-lookup kernel (k_lookup_piped; k_lookup_staged on unsorted tail queues): algorithmic bytes = 64 B per
             (lookup, nuclide) (grid pair + sigma_t/c/f pairs) / summed
             lookup time.  The staged kernel re-reads each record from shared
             memory for ~1000 particles, so achieved > HBM peak: the kernel is
@@ -84,7 +84,7 @@ def problem(args):
         return P.depleted_pincell(12, 3, 100, 8, seed=1)
     return P.depleted_pincell(272, 3, 11303, 100, seed=1)
 BYTES_PER_NUCLIDE_LOOKUP = 64
-TRAFFIC_PROFILE = "r1s4_lookup_traffic.json"
+TRAFFIC_PROFILE = "r1s5_lookup_traffic.json"
 
 
 def _peaks():
@@ -324,7 +324,7 @@ def run_ours(args):
         "gpu_launches": int(launches0["end"] - launches0["n"]),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "k_lookup_staged", "peak_source": peak_src,
+                     "kernel": "k_lookup_piped", "peak_source": peak_src,
                      "algorithmic_bytes": "64 B x nuclide-lookups (grid pair + sigma_t,c,f pairs)",
                      "nuclide_lookups_per_step": n_nl / args.steps},
         "clocks": sampler.summary(),

@@ -485,10 +485,11 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                                 snf[p] = __dadd_rn(snf[p], __dmul_rn(dd.y, ff[p]));
                             }
                         }
-                        // prefix checkpoint after every kCkptStride (= 2 stages) nuclides
-                        static_assert(kCkptStride == 2 * LK_G, "checkpoint every second stage");
-                        if (ckon && (t & 1) && (t + 1) * LK_G <= ncomp) {
-                            const int32_t row = t >> 1;
+                        // prefix checkpoint after every kCkptStride nuclides (whole stages)
+                        static_assert(kCkptStride % LK_G == 0, "checkpoints at stage boundaries");
+                        constexpr int CKS = kCkptStride / LK_G;
+                        if (ckon && (t + 1) % CKS == 0 && (t + 1) * LK_G <= ncomp) {
+                            const int32_t row = (t + 1) / CKS - 1;
 #pragma unroll
                             for (int p = 0; p < PPL; ++p) {
                                 double* ckb = MODE == 0 ? S.ckpt + s[p] : bout + n + i[p];
@@ -747,8 +748,9 @@ __global__ void __launch_bounds__(1024, 1)
                         sf = __dadd_rn(sf, __dmul_rn(dd.x, ff));
                         snf = __dadd_rn(snf, __dmul_rn(dd.y, ff));
                     }
-                    if (ckon && (t & 1) && (t + 1) * LK_G <= ncomp) {
-                        const int32_t row = t >> 1;
+                    constexpr int CKS = kCkptStride / LK_G;
+                    if (ckon && (t + 1) % CKS == 0 && (t + 1) * LK_G <= ncomp) {
+                        const int32_t row = (t + 1) / CKS - 1;
                         double* ckb = MODE == 0 ? S.ckpt + s : bout + n + i;
                         if (mine && row < nck) ckb[(int64_t)row * cks] = st;
                     }

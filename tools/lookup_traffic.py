@@ -1,7 +1,7 @@
 """DRAM bytes per nuclide-lookup of the staged lookup kernel over one whole
 C4 batch (40M particles): sums ncu's per-launch dram bytes (CSV from
 `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum
--k regex:k_lookup_staged --csv --log-file X python tools/profile_step.py`) and
+-k regex:"k_lookup_(piped|staged)" --csv --log-file X python tools/profile_step.py`) and
 divides by the batch's nuclide-lookups printed by profile_step.
 
     python tools/lookup_traffic.py <ncu.csv> <profile_step.log> <out.json>
@@ -29,7 +29,7 @@ timings = ast.literal_eval(log[log.index("timings ") + 8:].strip().splitlines()[
 nl = timings["nuclide_lookups_active"]
 dram = tot["dram__bytes_read.sum"] + tot["dram__bytes_write.sum"]
 out = {"capture": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum over every "
-                  "k_lookup_staged launch of one C4 batch (tools/profile_step.py --particles 40000000)",
+                  "k_lookup_piped/k_lookup_staged launch of one C4 batch (tools/profile_step.py --particles 40000000)",
        "launches": len(ids), "nuclide_lookups": nl, "dram_bytes": dram,
        "dram_bytes_read": tot["dram__bytes_read.sum"], "dram_bytes_write": tot["dram__bytes_write.sum"],
        "dram_bytes_per_nuclide_lookup": dram / nl, "algorithmic_bytes_per_nuclide_lookup": 64,
