@@ -146,8 +146,9 @@ struct emc_ctx {
     int lookup_block = 1024;
     bool staged = true;          // k_lookup_staged + energy-major sort (EMC_LOOKUP=plain: k_lookup)
     size_t lk_smem = 0;
-    int lk_cfg = 0;              // staged-lookup launch configuration (EMC_LK_CFG)
+    int lk_cfg = 2;              // chunk-synchronous staged lookup (tail queues) launch configuration (EMC_LK_CFG)
     bool lk_piped = true;        // chunk-pipelined staged lookup on sorted queues (EMC_LK_PIPED)
+    int lk_pcfg = 1;             // its CTA configuration (EMC_LK_PCFG: 0 = 32 warps x 1, 1 = 16 warps x 2, 2 = 10 x 3)
     DSlots S{};
 
     // queues + sort scratch
@@ -528,6 +529,8 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
     if (const char* lk = getenv("EMC_LOOKUP")) c->staged = std::strcmp(lk, "plain") != 0;
     c->lk_piped = true;
     if (const char* lp = getenv("EMC_LK_PIPED")) c->lk_piped = atoi(lp) != 0;
+    c->lk_pcfg = 1;
+    if (const char* lp = getenv("EMC_LK_PCFG")) c->lk_pcfg = std::max(0, std::min(2, atoi(lp)));
     const char* ro = getenv("EMC_REORDER");
     c->reorder = !(ro && ro[0] == '0');
     if (c->reorder) rc |= c->ps2.alloc(nslots);
@@ -572,6 +575,7 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
             if (const char* e = getenv("EMC_SORT_FINE")) c->band_bits = std::max(0, std::min(12, atoi(e)));
         }
         c->mat_bits = bits(c->n_materials);
+        if (c->staged) if (const char* e = getenv("EMC_SORT_MAT")) if (atoi(e) == 0) c->mat_bits = 0;
         c->ebin_bits = bits(c->L.nbins);
         int total = c->grp_bits + c->band_bits + c->mat_bits + c->ebin_bits;
         if (total > 32) {            // drop fine-energy bits first (order stays valid)
@@ -827,7 +831,8 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
                 if (do_sort && c->reorder) rdst = c->ps_cur == c->ps.p ? c->ps2.p : c->ps.p;
                 if (do_sort && c->lk_piped)
                     EMC_TRY_CUDA(lk_launch_piped<0>(c->L, q, nL, c->S, cf.fused, c->cnt.p, nullptr, nullptr, nullptr,
-                                                    c->sm_count, c->lk_smem, st, rdst, lk_keys(c, c->keys_out.p)));
+                                                    c->sm_count, c->lk_smem, st, rdst, lk_keys(c, c->keys_out.p),
+                                                    c->lk_pcfg));
                 else
                     EMC_TRY_CUDA(lk_launch<0>(c->lk_cfg, c->L, q, nL, c->S, cf.fused, c->cnt.p, nullptr, nullptr,
                                               nullptr, c->sm_count, c->lk_smem, st, nullptr, rdst));

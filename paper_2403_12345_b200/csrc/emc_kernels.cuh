@@ -61,7 +61,7 @@ __device__ __forceinline__ uint32_t lookup_key(const DLib& L, const QKeys& K, do
     const uint32_t eb = (uint32_t)energy_bin(E, L);
     uint32_t k = (uint32_t)__ldg(L.mat_group + m);
     k = K.ebin_bits ? ((k << K.ebin_bits) | (eb >> K.ebin_shift)) : k;
-    k = (k << K.mat_bits) | (uint32_t)m;
+    if (K.mat_bits) k = (k << K.mat_bits) | (uint32_t)m;
     if (K.fine_bits) {
         const uint64_t e64 = (uint64_t)__double_as_longlong(E);
         k = (k << K.fine_bits) | (uint32_t)((e64 >> (L.shift - K.fine_bits)) & ((1u << K.fine_bits) - 1u));

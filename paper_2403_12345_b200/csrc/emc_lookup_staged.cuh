@@ -27,10 +27,16 @@ namespace emc {
 // CTA = NW warps: NW-1 consumer warps (one particle per lane; a chunk is
 // (NW-1)*32 consecutive queue entries) + 1 producer warp; MINB CTAs per SM.
 constexpr int LK_G = 8;                    // nuclides per pipeline stage
-constexpr int LK_D = 6;                    // stages in flight
+#ifndef EMC_LK_D
+#define EMC_LK_D 3
+#endif
+constexpr int LK_D = EMC_LK_D;             // stages in flight (3: two CTAs fit per SM; 6 for one)
 constexpr int LK_R = 16;                   // staged interval records per nuclide window
 constexpr int LK_SCAN = 4;                 // wider windows start the scan at the hash bound
-constexpr int LK_MIN_NUC = 16;             // smaller groups use the direct path
+#ifndef EMC_LK_MIN_NUC
+#define EMC_LK_MIN_NUC 16
+#endif
+constexpr int LK_MIN_NUC = EMC_LK_MIN_NUC;  // smaller groups use the direct path
 constexpr int LK_DS = 2 * LK_G + 2;        // doubles per material in a density block: 8 (den, den*nu)
                                            // pairs; the 144-byte stride spreads materials over banks
 constexpr int LK_DEN_BYTES_MAX = 150 * 1024;
@@ -555,13 +561,13 @@ __host__ __device__ constexpr size_t lk_pipe_offset(int n_mat, int den_staged)
     return (lk_smem_bytes(n_mat, den_staged) + 15) & ~(size_t)15;
 }
 
-template <int MODE, bool DEN_ST>
-__global__ void __launch_bounds__(1024, 1)
+template <int MODE, bool DEN_ST, int NW, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB)
     k_lookup_piped(const int32_t* __restrict__ q, int32_t n, DLib L, DSlots S, int32_t fused,
                    unsigned long long* cnt, const double* __restrict__ bE, const int32_t* __restrict__ bM,
                    double* __restrict__ bout, PState* __restrict__ rdst, LkKeys K)
 {
-    constexpr int NW = 32, LK_CONS = NW - 1, LK_CHUNK = LK_CONS * 32;
+    constexpr int LK_CONS = NW - 1, LK_CHUNK = LK_CONS * 32;
     extern __shared__ __align__(128) unsigned char lk_raw[];
     LkShared& sh = *reinterpret_cast<LkShared*>(lk_raw);
     double* const sden = reinterpret_cast<double*>(lk_raw + sizeof(LkShared));
@@ -777,27 +783,49 @@ __global__ void __launch_bounds__(1024, 1)
     }
 }
 
+// piped configurations: 0 = one 32-warp CTA per SM, 1 = two 16-warp CTAs per SM
+// (their chunk boundaries overlap; needs the ring to fit twice in shared memory)
+constexpr int lk_pcfg_warps(int c) { return c == 1 ? 16 : c == 2 ? 10 : 32; }
+constexpr int lk_pcfg_minb(int c) { return c == 1 ? 2 : c == 2 ? 3 : 1; }
+
+template <int MODE, int PC>
+inline cudaError_t lk_launch_piped_cfg(const DLib& L, const int32_t* q, int64_t n, DSlots S, int32_t fused,
+                                       unsigned long long* cnt, const double* bE, const int32_t* bM, double* bout,
+                                       int sm_count, size_t smem, cudaStream_t st, PState* rdst, const LkKeys& K)
+{
+    constexpr int NW = lk_pcfg_warps(PC), MB = lk_pcfg_minb(PC);
+    constexpr int64_t chunk = (NW - 1) * 32;
+    const unsigned nb = (unsigned)std::min<int64_t>((n + chunk - 1) / chunk, (int64_t)sm_count * MB);
+    if (L.den_staged)
+        k_lookup_piped<MODE, true, NW, MB><<<nb, NW * 32, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM, bout,
+                                                                      rdst, K);
+    else
+        k_lookup_piped<MODE, false, NW, MB><<<nb, NW * 32, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM, bout,
+                                                                       rdst, K);
+    return cudaGetLastError();
+}
+
 template <int MODE>
 inline cudaError_t lk_launch_piped(const DLib& L, const int32_t* q, int64_t n, DSlots S, int32_t fused,
                                    unsigned long long* cnt, const double* bE, const int32_t* bM, double* bout,
-                                   int sm_count, size_t smem, cudaStream_t st, PState* rdst, const LkKeys& K)
+                                   int sm_count, size_t smem, cudaStream_t st, PState* rdst, const LkKeys& K,
+                                   int pcfg = 0)
 {
-    constexpr int64_t chunk = 31 * 32;
-    const unsigned nb = (unsigned)std::min<int64_t>((n + chunk - 1) / chunk, (int64_t)sm_count);
-    if (L.den_staged)
-        k_lookup_piped<MODE, true><<<nb, 1024, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM, bout, rdst, K);
-    else
-        k_lookup_piped<MODE, false><<<nb, 1024, smem, st>>>(q, (int32_t)n, L, S, fused, cnt, bE, bM, bout, rdst, K);
-    return cudaGetLastError();
+    if (pcfg == 1)
+        return lk_launch_piped_cfg<MODE, 1>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, rdst, K);
+    if (pcfg == 2)
+        return lk_launch_piped_cfg<MODE, 2>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, rdst, K);
+    return lk_launch_piped_cfg<MODE, 0>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, rdst, K);
 }
 
 }  // namespace emc
 
 namespace emc {
 
-// Launch configurations of the staged lookup (warps per CTA x CTAs per SM x
-// particles per lane).  EMC_LK_CFG selects one at run time (tuning); 0 is
-// the default.
+// Launch configurations of the chunk-synchronous staged lookup (warps per CTA
+// x CTAs per SM x particles per lane), used on the unsorted tail queues.
+// EMC_LK_CFG selects one at run time (tuning); 2 (two 16-warp CTAs per SM,
+// which the 3-stage ring lets fit) is the default.
 constexpr int LK_NCFG = 4;
 constexpr int lk_cfg_warps(int c) { return c == 1 ? 20 : c == 2 ? 16 : c == 3 ? 17 : 32; }
 constexpr int lk_cfg_minb(int c) { return c == 1 || c == 2 ? 2 : 1; }
@@ -854,10 +882,18 @@ inline cudaError_t lk_set_smem(size_t smem)
         (e = lk_set_smem_cfg<1, 2>(smem)) || (e = lk_set_smem_cfg<1, 3>(smem)))
         return e;
     const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
-    if ((e = cudaFuncSetAttribute(k_lookup_piped<0, true>, a, (int)smem)) ||
-        (e = cudaFuncSetAttribute(k_lookup_piped<0, false>, a, (int)smem)) ||
-        (e = cudaFuncSetAttribute(k_lookup_piped<1, true>, a, (int)smem)) ||
-        (e = cudaFuncSetAttribute(k_lookup_piped<1, false>, a, (int)smem)))
+    if ((e = cudaFuncSetAttribute(k_lookup_piped<0, true, 32, 1>, a, (int)smem)) ||
+        (e = cudaFuncSetAttribute(k_lookup_piped<0, false, 32, 1>, a, (int)smem)) ||
+        (e = cudaFuncSetAttribute(k_lookup_piped<1, true, 32, 1>, a, (int)smem)) ||
+        (e = cudaFuncSetAttribute(k_lookup_piped<1, false, 32, 1>, a, (int)smem)) ||
+        (e = cudaFuncSetAttribute(k_lookup_piped<0, true, 16, 2>, a, (int)smem)) ||
+        (e = cudaFuncSetAttribute(k_lookup_piped<0, false, 16, 2>, a, (int)smem)) ||
+        (e = cudaFuncSetAttribute(k_lookup_piped<1, true, 16, 2>, a, (int)smem)) ||
+        (e = cudaFuncSetAttribute(k_lookup_piped<1, false, 16, 2>, a, (int)smem)) ||
+        (e = cudaFuncSetAttribute(k_lookup_piped<0, true, 10, 3>, a, (int)smem)) ||
+        (e = cudaFuncSetAttribute(k_lookup_piped<0, false, 10, 3>, a, (int)smem)) ||
+        (e = cudaFuncSetAttribute(k_lookup_piped<1, true, 10, 3>, a, (int)smem)) ||
+        (e = cudaFuncSetAttribute(k_lookup_piped<1, false, 10, 3>, a, (int)smem)))
         return e;
     return cudaSuccess;
 }
