@@ -97,22 +97,26 @@ def _peaks():
 
 
 class ClockSampler:
-    """Clocks/throttle sampling during the timed region: NVML in-process (the
-    library behind nvidia-smi), else `nvidia-smi --query-gpu` (BENCH_CLOCKS=smi)."""
+    """Clocks/throttle sampling over the timed region: NVML in-process (the
+    library behind nvidia-smi), else `nvidia-smi --query-gpu` (BENCH_CLOCKS=smi).
+    The sampling thread is started before the run (its NVML initialisation must
+    not land inside the timed region of short batches); `mark()` brackets the
+    timed region and only samples inside it (or the two nearest ones, for
+    regions shorter than the sampling period) are reported."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    PERIOD = 0.05
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.rows = []
+        self.rows = []            # (monotonic time, fields)
+        self.window = [None, None]
         self._stop = threading.Event()
         self._t = None
 
     def _run_nvml(self):
-        # the library nvidia-smi reads: same fields without spawning a process
-        # (and re-initialising NVML) every sample, which stalls short batches
         import pynvml as nv
         nv.nvmlInit()
         try:
@@ -123,11 +127,12 @@ class ClockSampler:
                     r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
                 except AttributeError:
                     r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                self.rows.append([str(self.gpu), str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
-                                  str(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)),
-                                  str(nv.nvmlDeviceGetPowerUsage(h) / 1000.0), hex(r)]
-                                 + ["Active" if r & b else "Not Active" for b in bits])
-                self._stop.wait(0.2)
+                self.rows.append((time.monotonic(),
+                                  [str(self.gpu), str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                   str(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)),
+                                   str(nv.nvmlDeviceGetPowerUsage(h) / 1000.0), hex(r)]
+                                  + ["Active" if r & b else "Not Active" for b in bits]))
+                self._stop.wait(self.PERIOD)
         finally:
             nv.nvmlShutdown()
 
@@ -144,35 +149,44 @@ class ClockSampler:
                                       f"--query-gpu={self.FIELDS}"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
                 if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
+                    self.rows.append((time.monotonic(), [c.strip() for c in out.split(",")]))
             except Exception:  # noqa: BLE001
                 pass
             self._stop.wait(0.2)
 
-    def __enter__(self):
+    def start(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
 
-    def __exit__(self, *a):
+    def mark(self, which: int):
+        self.window[which] = time.monotonic()
+
+    def stop(self):
         self._stop.set()
         if self._t:
             self._t.join(timeout=6)
 
     def summary(self):
-        if not self.rows:
+        t0, t1 = self.window
+        rows = [r for ts, r in self.rows if t0 is not None and t1 is not None and t0 <= ts <= t1]
+        if not rows and self.rows and t0 is not None:
+            before = [r for ts, r in self.rows if ts < t0][-1:]
+            after = [r for ts, r in self.rows if t1 is not None and ts > t1][:1]
+            rows = before + after
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         reasons = set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for r in self.rows:
+        for r in rows:
             for name, v in zip(names, r[5:9]):
                 if v.strip().lower() == "active":
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.rows)}
+                "samples": len(rows)}
 
 
 def init_dist():
@@ -266,14 +280,14 @@ def run_ours(args):
     eng.set_stream(stream.cuda_stream)
     ev = {}
     launches0 = {}
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local).start()
 
     def on_batch(b, phase, e):
         if b == args.warmup and phase == "start":
             if torch.distributed.is_initialized():
                 torch.distributed.barrier()
             torch.cuda.synchronize()
-            sampler.__enter__()
+            sampler.mark(0)
             ev["start"] = torch.cuda.Event(enable_timing=True)
             ev["start"].record(stream)
             launches0["n"] = e.launch_count
@@ -282,9 +296,12 @@ def run_ours(args):
             ev["end"].record(stream)
             torch.cuda.synchronize()
             launches0["end"] = e.launch_count
-            sampler.__exit__()
+            sampler.mark(1)
 
-    res = P.run_event(cfg, lib, cell, on_batch=on_batch)
+    try:
+        res = P.run_event(cfg, lib, cell, on_batch=on_batch)
+    finally:
+        sampler.stop()
     dev_ms = ev["start"].elapsed_time(ev["end"])
     if torch.distributed.is_initialized():
         t = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")

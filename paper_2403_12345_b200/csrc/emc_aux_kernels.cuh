@@ -57,33 +57,53 @@ __global__ void k_log_keys(const int64_t* __restrict__ gid, const int32_t* __res
 }
 
 // one thread per bin: sequential left fold of its segment, starting from init
-__global__ void k_log_fold(const uint64_t* __restrict__ keys, const double* __restrict__ vals, int64_t n,
-                           int shift, int32_t n_bins, const double* __restrict__ init,
-                           double* __restrict__ out)
+// One CTA per bin: the bin's value range (binary-searched in the sorted keys)
+// is streamed through shared memory in tiles by the whole CTA (coalesced,
+// double-buffered) while thread 0 runs the left fold -- the order-defining,
+// inherently serial add chain -- out of shared memory.
+constexpr int LF_THREADS = 256, LF_TILE = 2048;
+
+__global__ void __launch_bounds__(LF_THREADS) k_log_fold(const uint64_t* __restrict__ keys,
+                                                         const double* __restrict__ vals, int64_t n, int shift,
+                                                         int32_t n_bins, const double* __restrict__ init,
+                                                         double* __restrict__ out)
 {
-    int32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ double tile[2][LF_TILE];
+    __shared__ int64_t rng[2];
+    const int32_t b = blockIdx.x;
     if (b >= n_bins) return;
-    // [first key with bin >= b, first key with bin >= b + 1): the left fold over
-    // the range then has no load-dependent exit, so value loads run ahead of the
-    // (inherently serial, order-defining) add chain
-    int64_t r[2];
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
+    if (threadIdx.x < 2) {                     // [first key with bin >= b, first key with bin >= b + 1)
         int64_t lo = 0, hi = n;
-        while (lo < hi) { int64_t mid = (lo + hi) >> 1; if ((int64_t)(keys[mid] >> shift) < b + k) lo = mid + 1; else hi = mid; }
-        r[k] = lo;
+        while (lo < hi) {
+            int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)(keys[mid] >> shift) < b + (int32_t)threadIdx.x) lo = mid + 1; else hi = mid;
+        }
+        rng[threadIdx.x] = lo;
     }
+    __syncthreads();
+    const int64_t r0 = rng[0], r1 = rng[1];
     double s = init[b];
-    int64_t e = r[0];
-    for (; e + 8 <= r[1]; e += 8) {
-        double v[8];
+    int buf = 0;
+    for (int64_t j = r0 + threadIdx.x; j < min(r1, r0 + LF_TILE); j += LF_THREADS) tile[0][j - r0] = vals[j];
+    __syncthreads();
+    for (int64_t t0 = r0; t0 < r1; t0 += LF_TILE) {
+        const int64_t t1 = min(r1, t0 + LF_TILE), n0 = t1 + LF_TILE;
+        // the other threads fetch the next tile while thread 0 folds this one
+        for (int64_t j = t1 + threadIdx.x; j < min(r1, n0); j += LF_THREADS) tile[buf ^ 1][j - t1] = vals[j];
+        if (threadIdx.x == 0) {
+            const double* v = tile[buf];
+            const int m = (int)(t1 - t0);
+            int k = 0;
+            for (; k + 8 <= m; k += 8) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = __ldg(vals + e + j);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) s = __dadd_rn(s, v[j]);
+                for (int u = 0; u < 8; ++u) s = __dadd_rn(s, v[k + u]);
+            }
+            for (; k < m; ++k) s = __dadd_rn(s, v[k]);
+        }
+        __syncthreads();
+        buf ^= 1;
     }
-    for (; e < r[1]; ++e) s = __dadd_rn(s, vals[e]);
-    out[b] = s;
+    if (threadIdx.x == 0) out[b] = s;
 }
 
 // stable replay key for reduce_batch(order="fast"): (bin, position)

@@ -168,8 +168,7 @@ struct emc_ctx {
     // contribution log
     DBuf<int64_t> lg_gid; DBuf<int32_t> lg_ord, lg_bin; DBuf<double> lg_val;
     int64_t log_n = 0;
-    int64_t prev_adv = 0, prev_logs = 0;   // last batch's advance events / log entries
-    bool prev_scored = false;
+    size_t log_want = 0;                  // capacity the next batch's log needs (presize_logs)
     DBuf<uint64_t> lkey_in, lkey_out; DBuf<double> lval_out;
     int gid_bits = 1;
 
@@ -554,8 +553,7 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
     if ((rc = alloc_sites(c, (size_t)(cfg->n_assigned * 2 + 4096)))) return rc;
     // both canonical banks up front (a run starts without a live source bank)
     if (c->banks[c->cur_bank].alloc(c->sites.parent.n)) return EMC_E_OOM;
-    c->prev_adv = c->prev_logs = 0;
-    c->prev_scored = false;
+    c->log_want = 0;
     if (cfg->use_logs) {
         if ((rc = alloc_logs(c, (size_t)(cfg->n_assigned * 64 + 4096)))) return rc;
     }
@@ -673,6 +671,21 @@ static LkKeys lk_keys(const emc_ctx* c, const uint32_t* keys)
     K.eb_mask = c->ebin_bits ? (uint32_t)((1ull << c->ebin_bits) - 1) : 0u;
     K.ebin_shift = c->ebin_shift;
     return K;
+}
+
+// grow the contribution log (and the CUB scratch of its sort) to c->log_want
+static int presize_logs(emc_ctx* c)
+{
+    const size_t want = c->log_want;
+    if (!c->cfg.use_logs || want <= c->lg_gid.n) return 0;
+    c->lg_gid.release(); c->lg_ord.release(); c->lg_bin.release(); c->lg_val.release();
+    c->lkey_in.release(); c->lkey_out.release(); c->lval_out.release();
+    if (int rc = alloc_logs(c, want)) return rc;
+    size_t need = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, need, c->lkey_in.p, c->lkey_out.p, c->lg_val.p, c->lval_out.p, (int)want,
+                                    0, 64, c->stream);
+    if (need > c->cub_tmp.n && c->cub_tmp.alloc(need)) return EMC_E_OOM;
+    return 0;
 }
 
 static int bits_for(int64_t v)
@@ -924,24 +937,7 @@ extern "C" int emc_run_batch(emc_ctx* c, const emc_batch_args* a, emc_batch_resu
     std::memset(res, 0, sizeof(*res));
     int64_t l0 = c->launches;
     int reruns = 0;
-    if (c->cfg.use_logs && c->prev_adv > 0) {
-        // size the contribution log from the previous batch before running, so
-        // the first scoring batch after the inactive ones does not overflow and
-        // rerun: an unscored batch logs only the k bin, a scored one up to 5
-        // entries per advance event more (K:617-640)
-        double est = (double)c->prev_logs + (c->prev_scored ? 0.0 : 5.0 * (double)c->prev_adv);
-        size_t want = (size_t)(1.25 * est) + 4096;
-        if (a->score && want > c->lg_gid.n) {
-            c->lg_gid.release(); c->lg_ord.release(); c->lg_bin.release(); c->lg_val.release();
-            c->lkey_in.release(); c->lkey_out.release(); c->lval_out.release();
-            int rc = alloc_logs(c, want);
-            if (rc) return rc;
-            size_t need = 0;
-            cub::DeviceRadixSort::SortPairs(nullptr, need, c->lkey_in.p, c->lkey_out.p, c->lg_val.p, c->lval_out.p,
-                                            (int)want, 0, 64, c->stream);
-            if (need > c->cub_tmp.n && c->cub_tmp.alloc(need)) return EMC_E_OOM;
-        }
-    }
+    if (int rc = presize_logs(c)) return rc;
     for (;;) {
         int rc = run_batch_once(c, a, res);
         if (rc) return rc;
@@ -966,9 +962,14 @@ extern "C" int emc_run_batch(emc_ctx* c, const emc_batch_args* a, emc_batch_resu
     }
     res->reruns = reruns;
     if (res->error) { res->launches = c->launches - l0; return 0; }
-    c->prev_adv = res->counters[CNT_EV_ADVANCE];
-    c->prev_logs = res->n_logs;
-    c->prev_scored = a->score != 0;
+    // capacity the next batch's contribution log needs: an unscored batch logs
+    // only the k bin, a scored one up to 5 entries per advance event more
+    // (K:617-640); grown after this batch's fold (emc_reduce_bins) or at the
+    // next batch's start, so the first scoring batch does not overflow and rerun
+    if (c->cfg.use_logs) {
+        const double est = (double)res->n_logs + (a->score ? 0.0 : 5.0 * (double)res->counters[CNT_EV_ADVANCE]);
+        c->log_want = (size_t)(1.25 * est) + 4096;
+    }
 
     // canonical bank: sort this rank's sites by (parent, ordinal)  (R:221-228)
     cudaStream_t st = c->stream;
@@ -1038,13 +1039,14 @@ extern "C" int emc_reduce_bins(emc_ctx* c, const double* init, double* out, int6
     else EMC_TRY_CUDA(cudaMemsetAsync(c->bins_init.p, 0, n_bins * 8, st));
     if (c->cfg.use_logs) {
         if (c->trace) EMC_TRY_CUDA(cudaEventRecord(c->ev[7], st));
-        k_log_fold<<<grid_for(n_bins, 128, 1 << 30), 128, 0, st>>>(c->lkey_out.p, c->lval_out.p, c->log_n,
+        k_log_fold<<<(unsigned)n_bins, LF_THREADS, 0, st>>>(c->lkey_out.p, c->lval_out.p, c->log_n,
                                                                     c->gid_bits + 17, (int32_t)n_bins,
                                                                     c->bins_init.p, c->bins_out.p);
         EMC_CHECK_LAUNCH(c);
         if (c->trace) EMC_TRY_CUDA(cudaEventRecord(c->ev[8], st));
         EMC_TRY_CUDA(cudaMemcpyAsync(out, c->bins_out.p, n_bins * 8, cudaMemcpyDeviceToHost, st));
         EMC_TRY_CUDA(cudaStreamSynchronize(st));
+        if (int rc = presize_logs(c)) return rc;   // this batch's log is folded: grow for the next
         if (c->trace) {
             float fm = 0;
             cudaEventElapsedTime(&fm, c->ev[7], c->ev[8]);
@@ -1259,8 +1261,10 @@ extern "C" int emc_replay_bins(emc_ctx* c, int64_t n, const int32_t* bin, const 
         int rc = sort_cub64(c, k1.p, k2.p, dv.p, dv2.p, n, pb + bb);
         if (rc) return rc;
     }
-    k_log_fold<<<grid_for(n_bins, 128, 1 << 30), 128, 0, st>>>(k2.p, dv2.p, n, pb, n_bins, dinit.p, dout.p);
-    EMC_CHECK_LAUNCH(c);
+    if (n_bins > 0) {
+        k_log_fold<<<(unsigned)n_bins, LF_THREADS, 0, st>>>(k2.p, dv2.p, n, pb, n_bins, dinit.p, dout.p);
+        EMC_CHECK_LAUNCH(c);
+    }
     to_host(sums, dout, n_bins, st);
     EMC_TRY_CUDA(cudaStreamSynchronize(st));
     db.release(); dv.release(); dv2.release(); k1.release(); k2.release(); dinit.release(); dout.release();
