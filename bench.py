@@ -107,7 +107,7 @@ class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-    PERIOD = 0.05
+    PERIOD = float(os.environ.get("BENCH_CLOCKS_PERIOD", "0.5"))   # faster polling perturbs short batches
 
     def __init__(self, gpu: int):
         self.gpu = gpu
@@ -137,6 +137,8 @@ class ClockSampler:
             nv.nvmlShutdown()
 
     def _run(self):
+        if os.environ.get("BENCH_CLOCKS") == "none":
+            return
         if os.environ.get("BENCH_CLOCKS", "nvml") == "nvml":
             try:
                 self._run_nvml()
