@@ -84,7 +84,7 @@ def problem(args):
         return P.depleted_pincell(12, 3, 100, 8, seed=1)
     return P.depleted_pincell(272, 3, 11303, 100, seed=1)
 BYTES_PER_NUCLIDE_LOOKUP = 64
-TRAFFIC_PROFILE = "r1s5_lookup_traffic.json"
+TRAFFIC_PROFILE = "r1s6_lookup_traffic.json"
 
 
 def _peaks():
@@ -339,7 +339,8 @@ def run_ours(args):
                        library_build_s=round(t_lib, 2)),
         "e2e": {"value": res.active_rate, "unit": "particles/s",
                 "h2d_bytes_per_step": res.timings.get("h2d_bytes_active", 0) / max(args.steps, 1),
-                "d2h_bytes_per_step": res.timings.get("d2h_bytes_active", 0) / max(args.steps, 1)},
+                "d2h_bytes_per_step": res.timings.get("d2h_bytes_active", 0) / max(args.steps, 1),
+                "d2h_bytes_final_bank": res.timings.get("d2h_bytes_final_bank", 0)},
         "gpu_launches": int(launches0["end"] - launches0["n"]),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,

@@ -209,7 +209,7 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
     else:
         cols = list(eng.bank_to_host())
     bank = FissionBank(*cols)
-    act["d2h_bytes_active"] += 68 * len(bank)
+    act["d2h_bytes_final_bank"] = 68 * len(bank)      # after the loop: not inside the active wall
 
     keff = KeffSeries(keff_values, config.inactive_batches)
     k_mean = k_stderr = tally_mean = tally_stderr = None
