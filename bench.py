@@ -121,6 +121,7 @@ class ClockSampler:
         nv.nvmlInit()
         try:
             h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+            mx = str(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))   # a slow query (ms): once
             bits = (0x8, 0x40, 0x20, 0x4)      # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
             while not self._stop.is_set():
                 try:
@@ -128,8 +129,7 @@ class ClockSampler:
                 except AttributeError:
                     r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
                 self.rows.append((time.monotonic(),
-                                  [str(self.gpu), str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
-                                   str(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)),
+                                  [str(self.gpu), str(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), mx,
                                    str(nv.nvmlDeviceGetPowerUsage(h) / 1000.0), hex(r)]
                                   + ["Active" if r & b else "Not Active" for b in bits]))
                 self._stop.wait(self.PERIOD)

@@ -182,6 +182,8 @@ struct emc_ctx {
     int64_t tail_n = 262144;
     bool trace = getenv("EMC_TRACE") != nullptr;   // per-iteration queue length / lookup time on stderr
     int tail_k = 16;
+    bool tail_plain = false;     // tail lookups with the one-particle-per-thread gather kernel (EMC_TAIL_LOOKUP=plain)
+    bool all_small = false;      // no composition group is staged (all < LK_MIN_NUC): the gather kernel serves
     cudaEvent_t evt[4 * 32]{};
     bool ev_init = false;
 };
@@ -210,6 +212,7 @@ extern "C" int emc_create(int device, emc_ctx** out)
     for (auto& e : c->evt) cudaEventCreate(&e);
     if (const char* t = getenv("EMC_TAIL_N")) c->tail_n = std::max<int64_t>(0, atoll(t));
     if (const char* t = getenv("EMC_TAIL_K")) c->tail_k = std::max(1, std::min(32, atoi(t)));
+    if (const char* t = getenv("EMC_TAIL_LOOKUP")) c->tail_plain = std::strcmp(t, "plain") == 0;
     c->ev_init = true;
     *out = c;
     return 0;
@@ -395,6 +398,9 @@ extern "C" int emc_upload_library(emc_ctx* c, const emc_library* lib)
         goff.release();
     }
     c->n_groups = (int32_t)sigs.size();
+    c->all_small = true;
+    for (size_t g = 0; g < sigs.size(); ++g)
+        if ((int32_t)sigs[g].size() >= LK_MIN_NUC) c->all_small = false;
     c->L = DLib{c->rec.p, c->ch_s.p, c->nu.p, c->mat_off.p, c->comp.p, c->hash.p, key_lo, (int32_t)nbins,
                 shift, lo, hi, c->mat_group.p, c->grp_off.p, c->gnuc.p, c->ddT.p, (int32_t)nm, 0,
                 c->iv.p, c->denS.p, den_staged, 0, c->nsafe.p};
@@ -778,8 +784,14 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
                     k_tail_begin<<<1, 1, 0, st>>>(c->ctl.p, c->cnt.p);
                     EMC_CHECK_LAUNCH(c);
                     EMC_TRY_CUDA(cudaEventRecord(c->evt[4 * k], st));
-                    EMC_TRY_CUDA(lk_launch<0>(c->lk_cfg, c->L, cur, nL, c->S, cf.fused, c->cnt.p, nullptr, nullptr,
-                                              nullptr, c->sm_count, c->lk_smem, st, &c->ctl.p->nLcur));
+                    if (c->tail_plain || c->all_small) {
+                        k_lookup<256><<<gl, 256, 0, st>>>(cur, (int32_t)nL, c->L, c->S, cf.fused, c->cnt.p,
+                                                          &c->ctl.p->nLcur);
+                        EMC_TRY_CUDA(cudaGetLastError());
+                    } else {
+                        EMC_TRY_CUDA(lk_launch<0>(c->lk_cfg, c->L, cur, nL, c->S, cf.fused, c->cnt.p, nullptr,
+                                                  nullptr, nullptr, c->sm_count, c->lk_smem, st, &c->ctl.p->nLcur));
+                    }
                     c->launches += 1;
                     EMC_TRY_CUDA(cudaEventRecord(c->evt[4 * k + 1], st));
                     k_advance<<<gl, BLK, 0, st>>>(cur, (int32_t)nL, bp, c->L, c->G, c->S, lg, c->bins.p, c->qc.p,
@@ -827,7 +839,7 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
                 if (rc) return rc;
                 q = c->qs.p;
                 host_cnt[CNT_SORTS] += 1;
-                if (c->reorder && !c->staged) {
+                if (c->reorder && (!c->staged || c->all_small)) {
                     PState* dst = c->ps_cur == c->ps.p ? c->ps2.p : c->ps.p;
                     k_reorder<<<grid_for(nL, BLK, 1 << 30), BLK, 0, st>>>(c->qs.p, (int32_t)nL, c->ps_cur, dst);
                     EMC_CHECK_LAUNCH(c);
@@ -838,7 +850,7 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             }
             look_inv++;
             EMC_TRY_CUDA(cudaEventRecord(c->ev[1], st));
-            if (c->staged) {
+            if (c->staged && !c->all_small) {
                 // the staged lookup moves the lines into sorted order itself (fused reorder)
                 PState* rdst = nullptr;
                 if (do_sort && c->reorder) rdst = c->ps_cur == c->ps.p ? c->ps2.p : c->ps.p;

@@ -236,8 +236,10 @@ __global__ void __launch_bounds__(256) k_reorder(const int32_t* __restrict__ per
 // share every grid record they gather through L1.
 template <int NT>
 __global__ void __launch_bounds__(NT, 1024 / NT) k_lookup(const int32_t* __restrict__ q, int32_t n, DLib L,
-                                                        DSlots S, int32_t fused, unsigned long long* cnt)
+                                                        DSlots S, int32_t fused, unsigned long long* cnt,
+                                                        const unsigned int* nptr = nullptr)
 {
+    if (nptr) n = (int32_t)*nptr;        // tail mode: queue length lives on the device
     unsigned long long nl = 0;
     EMC_WARP_LOOP(n) {
         int64_t i = emc_base_ + lane_id();

@@ -1,0 +1,5 @@
+run() { env $1 timeout 300 python bench.py --workload $2 --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$1 $2', round(d['value']/1e6,3), {k: round(v,4) for k,v in d['timings_s'].items() if k in ('advance','collision','lookup','sort')})"; }
+for w in c4 c3 c1 c5; do
+run EMC_TAIL_LOOKUP=staged $w
+run EMC_TAIL_LOOKUP=plain $w
+done
