@@ -257,6 +257,82 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_lookup(const int32_t* __restr
     warp_add_u64(cnt + CNT_NUCLIDE_LOOKUPS, nl);
 }
 
+// Warp-per-particle lookup for the sparse tail of a batch: a lone fuel
+// particle's 272-nuclide fold through the global path is ~272 dependent
+// gathers long, which sets the duration of every small tail iteration.  Here
+// the 32 lanes of a warp look up 32 nuclides of ONE particle at a time
+// (independent gathers), then every lane replays the reference's sequential
+// fold over those 32 values in composition order (shuffles; same operations,
+// same order as macro_tcf, so bit-identical sums and checkpoints).
+__global__ void __launch_bounds__(256) k_lookup_warp(const int32_t* __restrict__ q, int32_t n, DLib L, DSlots S,
+                                                     int32_t fused, unsigned long long* cnt,
+                                                     const unsigned int* nptr)
+{
+    if (nptr) n = (int32_t)*nptr;
+    const int lane = (int)(threadIdx.x & 31u);
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long nl = 0;
+    for (int64_t i = w0; i < n; i += nw) {
+        const int32_t s = q[i];
+        const double E = S.ps[s].a.E;
+        const int32_t m = S.ps[s].d.mat;
+        const int32_t grp = __ldg(L.mat_group + m);
+        const int32_t e0 = __ldg(L.grp_off + grp), ncomp = __ldg(L.grp_off + grp + 1) - e0;
+        const int32_t bin = energy_bin(E, L);
+        double* const ck = fused ? S.ckpt + s : nullptr;
+        double st = 0.0, sc = 0.0, sf = 0.0, snf = 0.0;
+        for (int32_t k0 = 0; k0 < ncomp; k0 += 32) {
+            double t = 0.0, cc = 0.0, f = 0.0, den = 0.0, dn = 0.0;
+            const int32_t k = k0 + lane;
+            if (k < ncomp) {
+                const NucRef r = L.gnuc[e0 + k];
+                const DD w = L.ddT[(int64_t)k * L.n_mat + m];
+                den = w.den; dn = w.dn;
+                const Rec* __restrict__ R = L.rec + r.g0;
+                const int32_t last = r.glen - 1;
+                if (last == 0) {
+                    const Rec r0 = R[0];
+                    t = r0.t; cc = r0.c; f = r0.f;
+                } else {
+                    int32_t j = __ldg(L.hash + r.hrow + bin);
+                    Rec r0 = R[j], r1 = R[j + 1];
+                    while (r1.E <= E && j + 1 < last) { ++j; r0 = r1; r1 = R[j + 1]; }
+                    if (j == 0 && E <= r0.E) { t = r0.t; cc = r0.c; f = r0.f; }
+                    else if (E >= r1.E) { t = r1.t; cc = r1.c; f = r1.f; }
+                    else {
+                        const double fr = frac(E, r0.E, r1.E);
+                        t = lerp(r0.t, r1.t, fr);
+                        cc = lerp(r0.c, r1.c, fr);
+                        f = lerp(r0.f, r1.f, fr);
+                    }
+                }
+            }
+            const int kn = min(32, ncomp - k0);
+            for (int j = 0; j < kn; ++j) {
+                const double tj = __shfl_sync(kFull, t, j), cj = __shfl_sync(kFull, cc, j);
+                const double fj = __shfl_sync(kFull, f, j), dj = __shfl_sync(kFull, den, j);
+                const double dnj = __shfl_sync(kFull, dn, j);
+                st = __dadd_rn(st, __dmul_rn(dj, tj));
+                sc = __dadd_rn(sc, __dmul_rn(dj, cj));
+                sf = __dadd_rn(sf, __dmul_rn(dj, fj));
+                snf = __dadd_rn(snf, __dmul_rn(dnj, fj));
+                if (ck && lane == 0 && ((k0 + j + 1) & (kCkptStride - 1)) == 0) {
+                    const int32_t row = (k0 + j + 1) / kCkptStride - 1;
+                    if (row < S.nck) ck[(int64_t)row * S.nslots] = st;
+                }
+            }
+        }
+        if (lane == 0) {
+            P2 c; c.t = st; c.c = sc; c.f = sf; c.nsf = snf;
+            S.ps[s].c = c;
+            nl += (unsigned long long)(__ldg(L.mat_off + m + 1) - __ldg(L.mat_off + m));
+        }
+    }
+    warp_add_u64(cnt + CNT_INTERP_TRANSPORT, 4ull * nl);
+    warp_add_u64(cnt + CNT_NUCLIDE_LOOKUPS, nl);
+}
+
 // Lookup microbenchmark kernel (tools/lookup_micro.py via emc_bench_lookup,
 // variant 4): the plain gather lookup (macro_tcf) over (mat, E) pairs; the
 // staged production kernel is variant 8 (k_lookup_staged<1, ...>).
