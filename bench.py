@@ -84,7 +84,7 @@ def problem(args):
         return P.depleted_pincell(12, 3, 100, 8, seed=1)
     return P.depleted_pincell(272, 3, 11303, 100, seed=1)
 BYTES_PER_NUCLIDE_LOOKUP = 64
-TRAFFIC_PROFILE = "r1s7_lookup_traffic.json"
+TRAFFIC_PROFILE = "r1s8_lookup_traffic.json"
 
 
 def _peaks():
