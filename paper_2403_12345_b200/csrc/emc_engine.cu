@@ -184,6 +184,7 @@ struct emc_ctx {
     int tail_k = 16;
     bool tail_plain = false;     // tail lookups with the one-particle-per-thread gather kernel (EMC_TAIL_LOOKUP=plain)
     int64_t tail_warp_n = 32768; // tail queues up to this length use the warp-per-particle lookup (EMC_TAIL_WARP_N)
+    int64_t tail_sub_n = 131072; // ... up to this length 8 lanes per particle (EMC_TAIL_SUB_N)
     bool all_small = false;      // no composition group is staged (all < LK_MIN_NUC): the gather kernel serves
     cudaEvent_t evt[4 * 32]{};
     bool ev_init = false;
@@ -215,6 +216,7 @@ extern "C" int emc_create(int device, emc_ctx** out)
     if (const char* t = getenv("EMC_TAIL_K")) c->tail_k = std::max(1, std::min(32, atoi(t)));
     if (const char* t = getenv("EMC_TAIL_LOOKUP")) c->tail_plain = std::strcmp(t, "plain") == 0;
     if (const char* t = getenv("EMC_TAIL_WARP_N")) c->tail_warp_n = std::max<int64_t>(0, atoll(t));
+    if (const char* t = getenv("EMC_TAIL_SUB_N")) c->tail_sub_n = std::max<int64_t>(0, atoll(t));
     c->ev_init = true;
     *out = c;
     return 0;
@@ -788,7 +790,12 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
                     EMC_TRY_CUDA(cudaEventRecord(c->evt[4 * k], st));
                     if (nL <= c->tail_warp_n) {
                         // sparse tail: one warp per particle (latency of one fold, not of 272 gathers)
-                        k_lookup_warp<<<grid_for(nL * 32, 256, 8 * c->sm_count), 256, 0, st>>>(
+                        k_lookup_warp<32><<<grid_for(nL * 32, 256, 8 * c->sm_count), 256, 0, st>>>(
+                            cur, (int32_t)nL, c->L, c->S, cf.fused, c->cnt.p, &c->ctl.p->nLcur);
+                        EMC_TRY_CUDA(cudaGetLastError());
+                    } else if (nL <= c->tail_sub_n) {
+                        // mid-size tail: 8 lanes per particle
+                        k_lookup_warp<8><<<grid_for(nL * 8, 256, 8 * c->sm_count), 256, 0, st>>>(
                             cur, (int32_t)nL, c->L, c->S, cf.fused, c->cnt.p, &c->ctl.p->nLcur);
                         EMC_TRY_CUDA(cudaGetLastError());
                     } else if (c->tail_plain || c->all_small) {

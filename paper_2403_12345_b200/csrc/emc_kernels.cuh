@@ -264,27 +264,41 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_lookup(const int32_t* __restr
 // (independent gathers), then every lane replays the reference's sequential
 // fold over those 32 values in composition order (shuffles; same operations,
 // same order as macro_tcf, so bit-identical sums and checkpoints).
+// LPP lanes per particle (32: one particle per warp; 8: four per warp for
+// mid-size tails).  Trip counts are made warp-uniform (the warp's longest
+// composition) so every shuffle is executed by all 32 lanes.
+template <int LPP>
 __global__ void __launch_bounds__(256) k_lookup_warp(const int32_t* __restrict__ q, int32_t n, DLib L, DSlots S,
                                                      int32_t fused, unsigned long long* cnt,
                                                      const unsigned int* nptr)
 {
+    constexpr int PPW = 32 / LPP;                 // particles per warp
     if (nptr) n = (int32_t)*nptr;
-    const int lane = (int)(threadIdx.x & 31u);
+    const int lane = (int)(threadIdx.x & 31u), sub = lane % LPP, grpl = lane / LPP;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long nl = 0;
-    for (int64_t i = w0; i < n; i += nw) {
-        const int32_t s = q[i];
-        const double E = S.ps[s].a.E;
-        const int32_t m = S.ps[s].d.mat;
-        const int32_t grp = __ldg(L.mat_group + m);
-        const int32_t e0 = __ldg(L.grp_off + grp), ncomp = __ldg(L.grp_off + grp + 1) - e0;
-        const int32_t bin = energy_bin(E, L);
-        double* const ck = fused ? S.ckpt + s : nullptr;
+    for (int64_t ib = w0 * PPW; ib < n; ib += nw * PPW) {
+        const int64_t i = ib + grpl;
+        const bool have = i < n;
+        int32_t s = 0, m = 0, e0 = 0, ncomp = 0, bin = 0;
+        double E = 1.0;
+        if (have) {
+            s = q[i];
+            E = S.ps[s].a.E;
+            m = S.ps[s].d.mat;
+            const int32_t grp = __ldg(L.mat_group + m);
+            e0 = __ldg(L.grp_off + grp);
+            ncomp = __ldg(L.grp_off + grp + 1) - e0;
+            bin = energy_bin(E, L);
+        }
+        int32_t nmax = ncomp;
+        for (int o = 16; o; o >>= 1) nmax = max(nmax, __shfl_xor_sync(kFull, nmax, o));
+        double* const ck = (fused && have) ? S.ckpt + s : nullptr;
         double st = 0.0, sc = 0.0, sf = 0.0, snf = 0.0;
-        for (int32_t k0 = 0; k0 < ncomp; k0 += 32) {
+        for (int32_t k0 = 0; k0 < nmax; k0 += LPP) {
             double t = 0.0, cc = 0.0, f = 0.0, den = 0.0, dn = 0.0;
-            const int32_t k = k0 + lane;
+            const int32_t k = k0 + sub;
             if (k < ncomp) {
                 const NucRef r = L.gnuc[e0 + k];
                 const DD w = L.ddT[(int64_t)k * L.n_mat + m];
@@ -308,22 +322,24 @@ __global__ void __launch_bounds__(256) k_lookup_warp(const int32_t* __restrict__
                     }
                 }
             }
-            const int kn = min(32, ncomp - k0);
+            const int kn = min(LPP, nmax - k0);
             for (int j = 0; j < kn; ++j) {
-                const double tj = __shfl_sync(kFull, t, j), cj = __shfl_sync(kFull, cc, j);
-                const double fj = __shfl_sync(kFull, f, j), dj = __shfl_sync(kFull, den, j);
-                const double dnj = __shfl_sync(kFull, dn, j);
-                st = __dadd_rn(st, __dmul_rn(dj, tj));
-                sc = __dadd_rn(sc, __dmul_rn(dj, cj));
-                sf = __dadd_rn(sf, __dmul_rn(dj, fj));
-                snf = __dadd_rn(snf, __dmul_rn(dnj, fj));
-                if (ck && lane == 0 && ((k0 + j + 1) & (kCkptStride - 1)) == 0) {
-                    const int32_t row = (k0 + j + 1) / kCkptStride - 1;
-                    if (row < S.nck) ck[(int64_t)row * S.nslots] = st;
+                const double tj = __shfl_sync(kFull, t, j, LPP), cj = __shfl_sync(kFull, cc, j, LPP);
+                const double fj = __shfl_sync(kFull, f, j, LPP), dj = __shfl_sync(kFull, den, j, LPP);
+                const double dnj = __shfl_sync(kFull, dn, j, LPP);
+                if (k0 + j < ncomp) {
+                    st = __dadd_rn(st, __dmul_rn(dj, tj));
+                    sc = __dadd_rn(sc, __dmul_rn(dj, cj));
+                    sf = __dadd_rn(sf, __dmul_rn(dj, fj));
+                    snf = __dadd_rn(snf, __dmul_rn(dnj, fj));
+                    if (ck && sub == 0 && ((k0 + j + 1) & (kCkptStride - 1)) == 0) {
+                        const int32_t row = (k0 + j + 1) / kCkptStride - 1;
+                        if (row < S.nck) ck[(int64_t)row * S.nslots] = st;
+                    }
                 }
             }
         }
-        if (lane == 0) {
+        if (have && sub == 0) {
             P2 c; c.t = st; c.c = sc; c.f = sf; c.nsf = snf;
             S.ps[s].c = c;
             nl += (unsigned long long)(__ldg(L.mat_off + m + 1) - __ldg(L.mat_off + m));
