@@ -309,3 +309,44 @@ def test_c4_full_size_statistical_parity():
         o = ores["batch_sums"][3:, score:500:5].sum(axis=1) / ocfg["particles_per_batch"]
         se = np.hypot(g.std(ddof=1) / np.sqrt(g.size), o.std(ddof=1) / np.sqrt(o.size))
         assert abs(g.mean() - o.mean()) < 4 * se, (score, g.mean(), o.mean(), se)
+
+
+_TAIL_VARIANT_SCRIPT = r"""
+import json, os, sys
+sys.path.insert(0, {tests!r}); sys.path.insert(0, {root!r})
+from conftest import GOLDEN, golden_library
+import paper_2403_12345_b200 as P
+g = json.load(open(os.path.join(GOLDEN, "golden.json")))
+out = {{}}
+for name in {runs!r}:
+    run = g["runs"][name]
+    pm = g["problems"][run["problem"]]
+    cell = P.Pincell(n_axial=pm["n_axial"], fuel_material_ids=pm["fuel_material_ids"],
+                     moderator_material_id=pm["moderator_material_id"])
+    res = P.run_replicated(P.RunConfig(**run["config"]), golden_library(run["problem"]), cell)
+    out[name] = res.physics_fingerprint()
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("env", [
+    {"EMC_TAIL_WARP_N": "0", "EMC_TAIL_SUB_N": "0"},                 # chunk-synchronous staged / gather
+    {"EMC_TAIL_WARP_N": "0", "EMC_TAIL_SUB_N": "1000000000"},        # 8 lanes per particle
+    {"EMC_TAIL_WARP_N": "1000000000"},                               # one warp per particle
+])
+def test_tail_lookup_variants_match_golden(golden, env):
+    """Every tail lookup kernel (small runs are mostly tail iterations) must
+    reproduce the reference's fingerprints; run in a fresh process because the
+    engine reads the thresholds when it is created."""
+    import json
+    import subprocess
+    import sys
+    runs = ["c1_event", "preset251_event_w2", "small_event_cap16"]
+    here = os.path.dirname(os.path.abspath(__file__))
+    code = _TAIL_VARIANT_SCRIPT.format(tests=here, root=os.path.dirname(here), runs=runs)
+    out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    got = json.loads(out.stdout.strip().splitlines()[-1])
+    for name in runs:
+        assert got[name] == golden["runs"][name]["fingerprint"], (name, env)
