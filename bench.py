@@ -44,9 +44,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "particles/s (active batches), HM-large depleted fuel, at 1/2/4/8 B200"
+GUARD_NOTE = ("box_guard on (RunConfig extension, include/emc.h): the reference's nudge can lose a particle "
+              "outside the reflective box (~1 per 1e9 histories; seed 42 stops batch 22 without it, "
+              "profiles/r2_c4_escape_replay.md); histories that stay inside are bit-identical to the reference")
 WORKLOAD = dict(workload="C4 HM-large depleted pincell: depleted_pincell(272,3,11303,100,seed=1)",
                 ppb_per_gpu=40_000_000, mode="event", reduction="fast", tally_mode="fused",
-                sort="on (group, log E, mat) every lookup sweep", seed=42)
+                sort="on (group, log E, mat) every lookup sweep", seed=42, box_guard=GUARD_NOTE)
 # --workload c5: BASELINE configs[4] (SURVEY 8f row 1 extension)
 METRIC_C5 = "particles/s (active batches), fixed-source shielding slab with 3D mesh flux tallies"
 WORKLOAD_C5 = dict(workload="C5 shielding_slab(8 nuclides/material, 2000 points, 12 layers, 60x60x60 cm, "
@@ -58,18 +61,18 @@ WORKLOAD_C5 = dict(workload="C5 shielding_slab(8 nuclides/material, 2000 points,
 # --workload c1: BASELINE configs[0] (the reference's own CPU-runnable case, SURVEY 8 "C1")
 METRIC_C1 = "particles/s (active batches), UO2 pincell, 12 fuel nuclides (C1)"
 WORKLOAD_C1 = dict(workload="C1 pincell: depleted_pincell(12,3,100,8,seed=1), 10k particles/batch", ppb_per_gpu=10_000,
-                   mode="event", reduction="deterministic", seed=42)
+                   mode="event", reduction="deterministic", seed=42, box_guard=GUARD_NOTE)
 # --workload c3: BASELINE configs[2] (Hoogenboom-Martin small restated on the pincell, SURVEY 8 "C3")
 METRIC_C3 = "particles/s (active batches), HM-small fresh fuel (34 fuel nuclides)"
-WORKLOAD_C3 = dict(workload="C3 HM-small pincell: depleted_pincell(34,3,11303,100,seed=1), 10M particles/batch; seed 7 "
-                            "(seed 42 hits the reference's own boundary GeometryError in batch 5, profiles/r1s5_c3_reference_error.txt)",
+WORKLOAD_C3 = dict(workload="C3 HM-small pincell: depleted_pincell(34,3,11303,100,seed=1), 10M particles/batch "
+                            "(seed 42 stops in batch 5 without the box guard, profiles/r1s5_c3_reference_error.txt)",
                    ppb_per_gpu=10_000_000,
-                   mode="event", reduction="fast", seed=7)
+                   mode="event", reduction="fast", seed=42, box_guard=GUARD_NOTE)
 # --workload c2: BASELINE configs[1] (17x17 assembly, SURVEY 8f row 2 extension)
 METRIC_C2 = "particles/s (active batches), 2D 17x17 PWR assembly, ~30 nuclides"
 WORKLOAD_C2 = dict(workload="C2 pwr_assembly(27 fuel + 3 moderator nuclides, 11303 points, 17x17 lattice, "
                             "25 water holes, 2D reflective), k-eigenvalue",
-                   ppb_per_gpu=1_000_000, mode="event", reduction="fast", seed=42)
+                   ppb_per_gpu=1_000_000, mode="event", reduction="fast", seed=42, box_guard=GUARD_NOTE)
 
 
 def problem(args):
@@ -84,7 +87,43 @@ def problem(args):
         return P.depleted_pincell(12, 3, 100, 8, seed=1)
     return P.depleted_pincell(272, 3, 11303, 100, seed=1)
 BYTES_PER_NUCLIDE_LOOKUP = 64
-TRAFFIC_PROFILE = "r1s8_lookup_traffic.json"
+# ncu counters of the XS-lookup kernels over one C4 batch of the CURRENT build
+# (tools/lookup_counters.py writes it with the hash of csrc/ it was captured on)
+LOOKUP_COUNTERS = "r2_lookup_counters.json"
+
+
+def csrc_hash() -> str:
+    import hashlib
+    h = hashlib.sha256()
+    d = os.path.join(ROOT, "paper_2403_12345_b200", "csrc")
+    for f in sorted(os.listdir(d)):
+        if f.endswith((".cu", ".cuh", ".h")):
+            with open(os.path.join(d, f), "rb") as fh:
+                h.update(f.encode() + fh.read())
+    return h.hexdigest()[:16]
+
+
+def lookup_counters(nl_per_step: float, launches_per_step: float) -> dict:
+    """The XS lookup's binding unit from ncu (profiles/LOOKUP_COUNTERS): DRAM
+    bytes and shared-memory wavefronts per nuclide-lookup, L1TEX throughput.
+    Counters cannot be read inside a timed run; the file records the source
+    hash it was captured on and `current` says whether that is this build."""
+    path = os.path.join(ROOT, "profiles", LOOKUP_COUNTERS)
+    try:
+        with open(path) as fh:
+            prof = json.load(fh)
+    except (OSError, ValueError):
+        return {"source": None}
+    out = {k: prof.get(k) for k in ("l1tex_throughput_pct", "dram_bytes_per_nuclide_lookup",
+                                     "shared_wavefronts_per_warp_nuclide", "design_min_wavefronts_per_warp_nuclide",
+                                     "fp64_pipe_pct", "issue_active_pct")}
+    out["unit"] = "L1TEX / shared-memory data pipe"
+    out["source"] = f"profiles/{LOOKUP_COUNTERS} ({prof.get('command', 'ncu')})"
+    out["current"] = prof.get("csrc_hash") == csrc_hash()
+    b = prof.get("dram_bytes_per_nuclide_lookup")
+    if b is not None and launches_per_step:
+        out["dram_bytes_per_launch"] = b * nl_per_step / launches_per_step
+    return out
 
 
 def _peaks():
@@ -205,25 +244,60 @@ def init_dist():
     return rank, ws, local
 
 
-def cpu_baseline(lib, cell, threads: int, ppb_sample: int, batches=(1, 2), ext=None) -> dict:
-    """The C oracle (restatement of the reference kernels, pinned bit-exact to
-    it) on this host's cores, W workers like run_replicated."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _oracle_ext(args, cell) -> dict:
+    """Oracle configuration of the workload's extensions (same as the GPU arm)."""
+    ext = {}
+    if args.workload == "c5":
+        ext = dict(run_mode="fixed_source", mesh=WORKLOAD_C5["mesh"], slab=True, vacuum=True)
+    else:
+        ext = dict(box_guard=True)
+    if cell.lattice > 1:
+        ext["lattice"] = (cell.lattice, cell.pitch, cell.pin_map)
+    return ext
+
+
+def _oracle_run(lib, cell, ext, threads, ppb, inactive, active, mode):
     from oracle import driver
-    cfg = dict(particles_per_batch=ppb_sample, inactive_batches=batches[0],
-               active_batches=batches[1], mode="event", max_in_flight=10000,
-               tally_mode="fused", reduction="deterministic", sort_enabled=True,
-               sort_every_n=1, seed=42, workers=threads, **(ext or {}))
-    res = driver.run(cfg, lib.arrays(), cell.as_tuple(), workers=threads)
-    return dict(value=res["active_rate"], unit="particles/s", cores=threads, kind="port",
-                sample=f"{'C5 slab' if ext and 'mesh' in ext else ('C2 assembly' if ext else 'C4')} library, "
-                       f"{ppb_sample} particles/batch x ({batches[0]} inactive + "
-                       f"{batches[1]} active), event mode, {threads} worker threads, "
-                       f"deterministic reduction (reference defaults)")
+    cfg = dict(particles_per_batch=ppb, inactive_batches=inactive, active_batches=active,
+               mode=mode, max_in_flight=10000, tally_mode="fused", reduction="deterministic",
+               sort_enabled=True, sort_every_n=1, seed=42, workers=threads, **ext)
+    return driver.run(cfg, lib.arrays(), cell.as_tuple(), workers=threads)
+
+
+def cpu_baseline(args, lib, cell, threads: int, ppb_sample: int, batches=(1, 2)) -> dict:
+    """The C oracle (restatement of the reference kernels, pinned bit-exact to
+    it) on this host's cores, W workers like run_replicated, in both of the
+    reference's executors; the faster one is the
+    baseline."""
+    ext = _oracle_ext(args, cell)
+    rates = {}
+    for mode in ("event", "history"):
+        res = _oracle_run(lib, cell, ext, threads, ppb_sample, batches[0], batches[1], mode)
+        rates[mode] = res["active_rate"]
+    best = max(rates, key=rates.get)
+    return dict(value=rates[best], unit="particles/s", cores=threads, kind="port", mode=best,
+                rates=rates, cpu_model=cpu_model(),
+                sample=f"{args.workload.upper()} library, {ppb_sample} particles/batch x ({batches[0]} inactive + "
+                       f"{batches[1]} active) in event and in history mode, {threads} worker threads, "
+                       f"deterministic reduction (reference defaults); value = the faster mode ({best})")
 
 
 def run_reference(args):
     """--impl reference: the reference's CPU path (oracle port; the reference
-    is Python/numba and cannot travel to the GPU box) on all host cores."""
+    is Python/numba and cannot travel to the GPU box) on all host cores, in
+    both of its executors (event: the reference default; history: CPU-optimal,
+    PAPER.md:70); the line reports the faster one."""
     rank, ws, _ = init_dist()
     if rank != 0:
         return
@@ -231,14 +305,12 @@ def run_reference(args):
     c5 = args.workload == "c5"
     threads = os.cpu_count() or 1
     ppb = args.ref_particles or (30000 if c5 else 3000) * threads
-    from oracle import driver
-    ext = dict(run_mode="fixed_source", mesh=WORKLOAD_C5["mesh"], slab=True, vacuum=True) if c5 else {}
-    if cell.lattice > 1:
-        ext["lattice"] = (cell.lattice, cell.pitch, cell.pin_map)
-    cfg = dict(particles_per_batch=ppb, inactive_batches=args.warmup, active_batches=args.steps,
-               mode="event", max_in_flight=10000, tally_mode="fused", reduction="deterministic",
-               sort_enabled=True, sort_every_n=1, seed=42, workers=threads, **ext)
-    res = driver.run(cfg, lib.arrays(), cell.as_tuple(), workers=threads)
+    ext = _oracle_ext(args, cell)
+    runs = {}
+    for mode in ("event", "history"):
+        runs[mode] = _oracle_run(lib, cell, ext, threads, ppb, args.warmup, args.steps, mode)
+    best = max(runs, key=lambda m: runs[m]["active_rate"])
+    res = runs[best]
     v = res["active_rate"]
     line = {"impl": "reference", "metric": {"c1": METRIC_C1, "c2": METRIC_C2, "c3": METRIC_C3, "c5": METRIC_C5}.get(args.workload, METRIC),
             "value": v, "unit": "particles/s",
@@ -247,12 +319,15 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": dict({"c1": WORKLOAD_C1, "c2": WORKLOAD_C2, "c3": WORKLOAD_C3, "c5": WORKLOAD_C5}.get(args.workload, WORKLOAD),
-                           reduction="deterministic (reference default)",
+                           mode=best, reduction="deterministic (reference default)",
                            ppb_sample=ppb,
                            impl="C restatement of the reference kernels (oracle/, bit-exact with the "
                                 "numba reference on this image's glibc)"),
             "cpu_baseline": {"value": v, "unit": "particles/s", "cores": threads, "kind": "port",
-                             "sample": f"{ppb} particles/batch x ({args.warmup}+{args.steps}) batches"},
+                             "cpu_model": cpu_model(), "mode": best,
+                             "rates": {m: r["active_rate"] for m, r in runs.items()},
+                             "sample": f"{ppb} particles/batch x ({args.warmup}+{args.steps}) batches, "
+                                       f"event and history executors, the faster reported"},
             "e2e": {"value": v, "unit": "particles/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -271,7 +346,7 @@ def run_ours(args):
     c5 = args.workload == "c5"
     wl = {"c1": WORKLOAD_C1, "c2": WORKLOAD_C2, "c3": WORKLOAD_C3, "c5": WORKLOAD_C5}.get(args.workload, WORKLOAD)
     ppb_gpu = args.particles or wl["ppb_per_gpu"]
-    ext = dict(run_mode="fixed_source", mesh=WORKLOAD_C5["mesh"]) if c5 else {}
+    ext = dict(run_mode="fixed_source", mesh=WORKLOAD_C5["mesh"]) if c5 else dict(box_guard=True)
     cfg = P.RunConfig(particles_per_batch=ppb_gpu * ws, inactive_batches=args.warmup,
                       active_batches=args.steps, mode="event", sort_enabled=True,
                       max_in_flight=args.max_in_flight or ppb_gpu, tally_mode="fused",
@@ -317,17 +392,7 @@ def run_ours(args):
     peak, peak_src = _peaks()
     lk_time = res.timings["lookup_active_s"] / ws if "lookup_active_s" in res.timings else None
     achieved = (BYTES_PER_NUCLIDE_LOOKUP * n_nl / ws) / lk_time / 1e9 if lk_time else None
-    # DRAM bytes per launch of the lookup kernel: ncu's dram__bytes_read+write
-    # summed over every lookup launch of one C4 batch, per nuclide-lookup
-    # (profiles/<round>_lookup_traffic.json), x this run's nuclide-lookups per launch
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", TRAFFIC_PROFILE)) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_nuclide_lookup")
-        if traffic is not None:
-            traffic = traffic * (n_nl / ws) / max(1, res.timings.get("lookup_launches_active", 1) / ws)
-    except Exception:  # noqa: BLE001
-        traffic = None
+    binding = lookup_counters(n_nl / ws, res.timings.get("lookup_launches_active", 0) / ws)
     line = {
         "metric": {"c1": METRIC_C1, "c2": METRIC_C2, "c3": METRIC_C3, "c5": METRIC_C5}.get(args.workload, METRIC), "value": value,
         "unit": "particles/s", "n_gpus": ws,
@@ -343,21 +408,27 @@ def run_ours(args):
                 "d2h_bytes_final_bank": res.timings.get("d2h_bytes_final_bank", 0)},
         "gpu_launches": int(launches0["end"] - launches0["n"]),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "k_lookup_piped", "peak_source": peak_src,
-                     "algorithmic_bytes": "64 B x nuclide-lookups (grid pair + sigma_t,c,f pairs)",
-                     "nuclide_lookups_per_step": n_nl / args.steps},
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": binding.pop("dram_bytes_per_launch", None),
+                     "kernel": "XS lookup: every lookup launch of the active batches (k_lookup_piped on sorted "
+                               "sweeps, k_lookup_staged / k_lookup_warp on unsorted tail queues), summed",
+                     "peak_source": peak_src,
+                     "algorithmic_bytes": "64 B x nuclide-lookups (grid pair + sigma_t,c,f pairs, SURVEY 8d)",
+                     "meaning": "north_star's HBM gather roofline: algorithmic gather bytes / lookup time vs HBM "
+                                "peak; frac > 1 because the staged kernel reads each record from DRAM once per "
+                                "chunk and serves ~1000 particles from shared memory. The binding unit is "
+                                "the L1TEX/shared-memory pipe (see 'binding')",
+                     "nuclide_lookups_per_step": n_nl / args.steps,
+                     "binding": binding},
         "clocks": sampler.summary(),
         "k_mean": res.k_mean, "k_stderr": res.k_stderr,
+        "box_guard_events": res.counters.get("box_guard"),
         "timings_s": {k: v for k, v in res.timings.items() if isinstance(v, float)},
     }
     if ws == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        oext = dict(ext, slab=cell.is_slab, vacuum=cell.boundary == "vacuum") if c5 else {}
-        if cell.lattice > 1:
-            oext["lattice"] = (cell.lattice, cell.pitch, cell.pin_map)
-        line["cpu_baseline"] = cpu_baseline(lib, cell, threads, args.cpu_particles or 1000 * threads,
-                                            ext=oext or None)
+        line["cpu_baseline"] = cpu_baseline(args, lib, cell, threads, args.cpu_particles or (
+            10000 if args.workload in ("c4", "c3") else 4000) * threads)
     if c5:
         line["mesh"] = {"cells": int(np.prod(WORKLOAD_C5["mesh"])),
                         "flux_first_layer": float(res.mesh_mean[0, ..., 0].sum()),
@@ -368,8 +439,8 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--particles", type=int, default=0,
                     help="particles per GPU per batch (default 40M for c4, 10M for c5)")

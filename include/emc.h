@@ -35,6 +35,16 @@ enum {
     EMC_E_RANGE = -4       /* problem exceeds an encoding limit */
 };
 
+/* Box guard (extension, off by default = the reference): the reference's
+ * reflect-and-nudge (kernels.py:782-797) and its DIST_EPS skip (K:418-492) can
+ * leave a particle just outside the reflective box; a fission site banked there
+ * stops the next batch with EMC_ERR_OUTSIDE_BOX (K:989-992).  With box_guard = 1
+ * a particle found outside the box after a move is put back on the box face it
+ * passed with that direction component pointing inward (vacuum geometry: it
+ * leaks).  Histories that stay inside are untouched, bit for bit; the number of
+ * guarded moves is counter EMC_CNT_BOX_GUARD. */
+#define EMC_CNT_BOX_GUARD 23
+
 /* transport error codes (kernels.py:108-113) */
 enum { EMC_ERR_NO_SURFACE = 1, EMC_ERR_OUTSIDE_BOX = 2, EMC_ERR_STREAM_OVERLAP = 3,
        EMC_ERR_RUNAWAY_HISTORY = 4, EMC_ERR_QUEUE_STATE = 5, EMC_ERR_NONPOSITIVE_SIGMA = 6 };
@@ -73,7 +83,7 @@ typedef struct {
     int32_t fused;                           /* tally_mode == "fused" */
     int32_t use_logs;                        /* reduction == "deterministic" */
     int32_t sort_enabled, sort_every;
-    int32_t pad;
+    int32_t box_guard;                       /* extension (RunConfig.box_guard), 0 = the reference */
     uint64_t seed;
     double alpha, fission_t;
     int64_t perturb_gid;                     /* -1: none */
@@ -164,6 +174,14 @@ int emc_bank_copy(emc_ctx *ctx, int64_t start, int64_t n, int64_t *parent, int32
 /* kernels.macro_lookup_full (kernels.py:287-331): sums[n][5], partials[n][max_comp][4] (nullable) */
 int emc_xs_lookup(emc_ctx *ctx, int64_t n, const int32_t *mats, const double *E, double *sums,
                   double *partials, int32_t max_comp);
+/* grid search of one composition entry (material entry k of mat_nuc, i.e. one
+ * nuclide's grid) at energy E, by the device's log-hash + forward scan
+ * (emc_device.cuh: bracket).  out[n][2] = (state, i): state 0 interior with
+ * grid[i] <= E < grid[i+1] (searchsorted(grid, E, 'right') - 1), 1 clamp to the
+ * first point (E <= grid[0], i = 0), 2 clamp to the last (E >= grid[-1],
+ * i = len-1) -- the reference's K:600-621 cases.  Parity hook for the grid
+ * indices north_star requires bit-exact. */
+int emc_grid_index(emc_ctx *ctx, int64_t n, const int32_t *entry, const double *E, int32_t *out);
 /* kernels.locate_point (kernels.py:403-415): out[n][3] = kind, axial, material */
 int emc_locate(emc_ctx *ctx, int64_t n, const double *pos, int32_t *out);
 /* kernels.boundary_distance (kernels.py:418-492): cell[n][2] = kind, axial */

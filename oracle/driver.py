@@ -67,7 +67,9 @@ class OGeom(C.Structure):
                 ("mx0", C.c_double), ("my0", C.c_double), ("mz0", C.c_double),
                 ("mdx", C.c_double), ("mdy", C.c_double), ("mdz", C.c_double),
                 ("lat_n", C.c_int32), ("n_pins", C.c_int32), ("pitch", C.c_double),
-                ("pin_map", P), ("pin_xy", P)]
+                ("pin_map", P), ("pin_xy", P),
+                # box guard extension (RunConfig.box_guard; include/emc.h)
+                ("guard", C.c_int32), ("gpad", C.c_int32)]
 
 
 class OSlots(C.Structure):
@@ -168,9 +170,9 @@ class OracleGeometry:
     With a mesh, ``self.mesh`` is this geometry's accumulator (one per worker:
     see OracleGeometry.for_worker)."""
 
-    def __init__(self, geom, slab=False, vacuum=False, mesh=None, lattice=None):
+    def __init__(self, geom, slab=False, vacuum=False, mesh=None, lattice=None, guard=False):
         radius, r2, hp, height, n_axial, zplanes, fuel_mats, mod_mat = geom
-        self.args = (geom, slab, vacuum, mesh, lattice)
+        self.args = (geom, slab, vacuum, mesh, lattice, guard)
         self.keep = [np.ascontiguousarray(zplanes, np.float64),
                      np.ascontiguousarray(fuel_mats, np.int32)]
         self.n_axial = int(n_axial)
@@ -192,7 +194,8 @@ class OracleGeometry:
             lat = (n, len(xy), pitch, _p(self.keep[2]), _p(self.keep[3]))
         self.s = OGeom(float(radius), float(r2), hp, height,
                        int(n_axial), _p(self.keep[0]), _p(self.keep[1]),
-                       int(mod_mat), int(bool(slab)), int(bool(vacuum)), mptr, *dims, *box, *lat)
+                       int(mod_mat), int(bool(slab)), int(bool(vacuum)), mptr, *dims, *box, *lat,
+                       int(bool(guard)), 0)
 
     def for_worker(self):
         return OracleGeometry(*self.args) if self.mesh is not None else self
@@ -355,7 +358,7 @@ def run(cfg: dict, lib_arrays, geom, workers: int | None = None,
     olib = OracleLibrary(lib_arrays)
     mesh = cfg.get("mesh")
     ogeom = OracleGeometry(geom, slab=cfg.get("slab", False), vacuum=cfg.get("vacuum", False),
-                           mesh=mesh, lattice=cfg.get("lattice"))
+                           mesh=mesh, lattice=cfg.get("lattice"), guard=cfg.get("box_guard", False))
     fixed = cfg.get("run_mode", "eigenvalue") == "fixed_source"
     ppb = int(cfg["particles_per_batch"])
     n_axial = ogeom.n_axial
@@ -448,7 +451,8 @@ def run(cfg: dict, lib_arrays, geom, workers: int | None = None,
             deaths = sum(int(w.counters[5]) + int(w.counters[6]) + int(w.counters[22]) for w in ws)
             if sourced != ppb or deaths != ppb:
                 raise OracleError("EventMCError", "neutron bookkeeping broken")
-            for name, idx in COUNTER_SUMS + ((("leaks", 22),) if cfg.get("vacuum") else ()):
+            for name, idx in COUNTER_SUMS + ((("leaks", 22),) if cfg.get("vacuum") else ()) + \
+                    ((("box_guard", 23),) if cfg.get("box_guard") else ()):
                 run_counters[name] = run_counters.get(name, 0) + sum(
                     int(w.counters[idx]) for w in ws)
             for name, idx in COUNTER_MAXES:

@@ -14,6 +14,9 @@
  * reference itself (tests/golden/make_golden.py).
  */
 #include <math.h>
+#ifdef ORACLE_TRACE
+#include <stdio.h>
+#endif
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -37,7 +40,7 @@ enum { CNT_LOG_N = 0, CNT_SITE_N, CNT_OVF, CNT_ERR, CNT_ERR_AUX, CNT_CAPTURES, C
        CNT_SOURCED, CNT_MAX_DRAWS, CNT_CLAMPS, CNT_INTERP_TRANSPORT, CNT_INTERP_SCORE,
        CNT_EV_LOOKUP, CNT_EV_ADVANCE, CNT_EV_COLLISION, CNT_INV_LOOKUP, CNT_INV_ADVANCE,
        CNT_INV_COLLISION, CNT_SORTS, CNT_MAX_INFLIGHT, CNT_MAX_HIST_LOG, CNT_NUCLIDE_LOOKUPS,
-       CNT_LEAKS };
+       CNT_LEAKS, CNT_BOX_GUARD };
 enum { ERR_NO_SURFACE = 1, ERR_OUTSIDE_BOX, ERR_STREAM_OVERLAP, ERR_RUNAWAY_HISTORY,
        ERR_QUEUE_STATE, ERR_NONPOSITIVE_SIGMA };
 enum { TM_LOOKUP = 0, TM_ADVANCE, TM_COLLISION, TM_SORT };
@@ -60,6 +63,8 @@ typedef struct {
     double mx0, my0, mz0, mdx, mdy, mdz;
     /* lattice extension: lat_n x lat_n pin cells of pitch */
     int32_t lat_n, n_pins; double pitch; const int32_t *pin_map; const double *pin_xy;
+    /* box guard (extension, RunConfig.box_guard; include/emc.h): 0 = the reference */
+    int32_t guard, gpad;
 } OGeom;
 
 typedef struct {
@@ -382,6 +387,34 @@ static void mesh_score(const OGeom *G, double x, double y, double z, double ux, 
     }
 }
 
+/* Box guard (extension, off by default; include/emc.h): the reference can
+ * leave a particle outside the reflective box -- e.g. an axial-plane crossing
+ * within 1e-9 of the cylinder nudges a fuel particle out of the cylinder while
+ * its cell stays fuel, and fuel cells never test the box planes (K:430-450,
+ * K:796-811).  A particle outside the closed box after a move is put back on
+ * the face it passed with that direction component pointing inward. */
+static int guard_fold(double *x, double *y, double *z, double *dx, double *dy, double *dz, const OGeom *G) {
+    int out = 0;
+    if (*x > G->hp) { *x = G->hp; if (*dx > 0.0) *dx = -*dx; out = 1; }
+    else if (*x < -G->hp) { *x = -G->hp; if (*dx < 0.0) *dx = -*dx; out = 1; }
+    if (*y > G->hp) { *y = G->hp; if (*dy > 0.0) *dy = -*dy; out = 1; }
+    else if (*y < -G->hp) { *y = -G->hp; if (*dy < 0.0) *dy = -*dy; out = 1; }
+    if (*z > G->height) { *z = G->height; if (*dz > 0.0) *dz = -*dz; out = 1; }
+    else if (*z < 0.0) { *z = 0.0; if (*dz < 0.0) *dz = -*dz; out = 1; }
+    return out;
+}
+/* ... then its cell is re-located and it goes back to the lookup queue (no
+ * collision at the guarded point); with vacuum planes it leaks. */
+static int guard_route(int64_t i, const OSlots *S, const OGeom *G, int64_t *cnt) {
+    cnt[CNT_BOX_GUARD] += 1;
+    if (G->vacuum) { cnt[CNT_LEAKS] += 1; return ROUTE_LEAK; }
+    int64_t loc[3];
+    oracle_locate(S->px[i], S->py[i], S->pz[i], G, loc);
+    S->kind[i] = (int8_t)loc[0]; S->axial[i] = (int32_t)loc[1]; S->mat[i] = (int32_t)loc[2];
+    return ROUTE_LOOKUP;
+}
+#define GUARD(i) (G->guard && guard_fold(&S->px[i], &S->py[i], &S->pz[i], &S->dx[i], &S->dy[i], &S->dz[i], G))
+
 /* K:713-811 */
 static int op_advance(int64_t i, const OSlots *S, const OLib *L, const OGeom *G, OLog *lg, double *wbins,
                       int64_t *cnt, int score, int fused, int use_logs) {
@@ -421,8 +454,13 @@ static int op_advance(int64_t i, const OSlots *S, const OLib *L, const OGeom *G,
         }
         if (G->mesh) mesh_score(G, S->px[i], S->py[i], S->pz[i], S->dx[i], S->dy[i], S->dz[i], ell, sig_t);
     }
+#ifdef ORACLE_TRACE   /* tools/c4_escape_replay.py --trace: one line per advance */
+    fprintf(stderr, "adv gid=%lld kind=%d ax=%d pos=(%.17g,%.17g,%.17g) dir=(%.17g,%.17g,%.17g) E=%.17g "
+            "d_coll=%.17g dist=%.17g surf=%lld\n", (long long)S->gid[i], S->kind[i], S->axial[i], S->px[i],
+            S->py[i], S->pz[i], S->dx[i], S->dy[i], S->dz[i], S->en[i], d_coll, dist, (long long)surf);
+#endif
     S->px[i] += S->dx[i] * ell; S->py[i] += S->dy[i] * ell; S->pz[i] += S->dz[i] * ell;
-    if (!crossing) return ROUTE_COLLISION;
+    if (!crossing) return GUARD(i) ? guard_route(i, S, G, cnt) : ROUTE_COLLISION;
     if (G->vacuum && surf >= SURF_XMIN && surf <= SURF_ZMAX) { cnt[CNT_LEAKS] += 1; return ROUTE_LEAK; }
     if (surf >= SURF_XMIN && surf <= SURF_ZMAX) {
         if (surf == SURF_XMIN || surf == SURF_XMAX) S->dx[i] = -S->dx[i];
@@ -438,7 +476,7 @@ static int op_advance(int64_t i, const OSlots *S, const OLib *L, const OGeom *G,
         S->axial[i] = (int32_t)(S->dz[i] > 0.0 ? jpl : jpl - 1);
     }
     S->mat[i] = S->kind[i] == KIND_FUEL ? G->fuel_mats[S->axial[i]] : (int32_t)G->mod_mat;
-    return ROUTE_LOOKUP;
+    return GUARD(i) ? guard_route(i, S, G, cnt) : ROUTE_LOOKUP;
 }
 
 /* K:814-923 */

@@ -41,7 +41,7 @@ class EmcRunConfig(C.Structure):
     _fields_ = [("particles_per_batch", _I64), ("gid_lo", _I64), ("n_assigned", _I64),
                 ("max_in_flight", _I64), ("history", _I32), ("fused", _I32),
                 ("use_logs", _I32), ("sort_enabled", _I32), ("sort_every", _I32),
-                ("pad", _I32), ("seed", C.c_uint64), ("alpha", _D), ("fission_t", _D),
+                ("box_guard", _I32), ("seed", C.c_uint64), ("alpha", _D), ("fission_t", _D),
                 ("perturb_gid", _I64)]
 
 
@@ -81,6 +81,7 @@ SYMBOLS = {
     "emc_bank_device": (C.c_int, [_P, C.POINTER(_P)]),
     "emc_bank_copy": (C.c_int, [_P, _I64, _I64] + [_P] * 9),
     "emc_xs_lookup": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I32]),
+    "emc_grid_index": (C.c_int, [_P, _I64, _P, _P, _P]),
     "emc_locate": (C.c_int, [_P, _I64, _P, _P]),
     "emc_distance": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P]),
     "emc_particle_ops": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P]),

@@ -117,6 +117,19 @@ __global__ void k_replay_keys(const int32_t* __restrict__ bin, int64_t n, int po
 
 // ----------------------------------------------------------- API kernels ---
 
+// emc_grid_index: (clamp state, local bracket index) of composition entry k at E
+__global__ void k_api_bracket(DLib L, int64_t n, const int32_t* __restrict__ entry,
+                              const double* __restrict__ E, int32_t* __restrict__ out)
+{
+    int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const Comp c = L.comp[entry[q]];
+    Rec r0, r1; int32_t gi;
+    const int st = bracket(L, c, energy_bin(E[q], L), E[q], gi, r0, r1);
+    out[2 * q] = st;
+    out[2 * q + 1] = gi - c.g0;
+}
+
 // K:287-331 macro_lookup_full: five sums + per-entry (t, s, c, f) partials
 __global__ void k_api_macro(DLib L, int64_t n, const int32_t* __restrict__ mats,
                             const double* __restrict__ E, int32_t max_comp, double* __restrict__ sums,

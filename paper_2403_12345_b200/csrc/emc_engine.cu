@@ -429,7 +429,7 @@ extern "C" int emc_upload_geometry(emc_ctx* c, const emc_geometry* g)
     EMC_TRY_CUDA(cudaMemcpy(c->zplanes.p, g->zplanes, (g->n_axial + 1) * 8, cudaMemcpyHostToDevice));
     EMC_TRY_CUDA(cudaMemcpy(c->fuel_mats.p, g->fuel_mats, g->n_axial * 4, cudaMemcpyHostToDevice));
     c->G = DGeom{g->radius, g->r2, g->half_pitch, g->height, (int32_t)g->n_axial, (int32_t)g->mod_mat,
-                 c->zplanes.p, c->fuel_mats.p, 0, 0, 1, 0, 0.0, nullptr, nullptr};
+                 c->zplanes.p, c->fuel_mats.p, 0, 0, 0, 0, 1, 0, 0.0, nullptr, nullptr};
     c->M.on = 0;
     c->n_bins = (int32_t)((g->n_axial + 1) * 5 + 1);
     c->kbin = c->n_bins - 1;
@@ -565,7 +565,11 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
     if (c->banks[c->cur_bank].alloc(c->sites.parent.n)) return EMC_E_OOM;
     c->log_want = 0;
     if (cfg->use_logs) {
-        if ((rc = alloc_logs(c, (size_t)(cfg->n_assigned * 64 + 4096)))) return rc;
+        // an unscored batch logs ~1 k-bin entry per collision (~4 per history at
+        // C4); later batches are presized from the previous one (log_want), so
+        // the log never holds the 64 entries per particle a scored batch may
+        // need before one has run (48 B per entry: ~120 GB at 40M particles)
+        if ((rc = alloc_logs(c, (size_t)(cfg->n_assigned * 8 + 4096)))) return rc;
     }
     // lookup sort key (32 bits): group | energy band | material | energy bin
     // (see k_sort_keys).  EMC_SORT_BANDS overrides the band count (1 = pure
@@ -611,7 +615,7 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
                                     (int32_t*)nullptr, (int)scap, 0, 64);
     if (cfg->use_logs)
         cub::DeviceRadixSort::SortPairs(nullptr, t3, (uint64_t*)nullptr, (uint64_t*)nullptr, (double*)nullptr,
-                                        (double*)nullptr, (int)c->lg_gid.n, 0, 64);
+                                        (double*)nullptr, (int64_t)c->lg_gid.n, 0, 64);
     if (c->cub_tmp.alloc(std::max<size_t>(std::max(t1, std::max(t2, t3)), 1))) return EMC_E_OOM;
     c->bank_n = 0;
     c->src = DSrc{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.0, 0};
@@ -663,9 +667,11 @@ template <class K, class V>
 static int sort_cub64(emc_ctx* c, const K* kin, K* kout, const V* vin, V* vout, int64_t n, int end_bit)
 {
     size_t need = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, need, kin, kout, vin, vout, (int)n, 0, end_bit, c->stream);
+    // 64-bit item count: a deterministic-mode contribution log passes 2^31
+    // entries at ~40M histories per rank (CUB's NumItemsT is templated)
+    cub::DeviceRadixSort::SortPairs(nullptr, need, kin, kout, vin, vout, n, 0, end_bit, c->stream);
     if (need > c->cub_tmp.n && c->cub_tmp.alloc(need)) return EMC_E_OOM;
-    EMC_TRY_CUDA(cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, need, kin, kout, vin, vout, (int)n, 0, end_bit,
+    EMC_TRY_CUDA(cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, need, kin, kout, vin, vout, n, 0, end_bit,
                                                  c->stream));
     c->launches += (end_bit + 7) / 8;
     return 0;
@@ -692,8 +698,8 @@ static int presize_logs(emc_ctx* c)
     c->lkey_in.release(); c->lkey_out.release(); c->lval_out.release();
     if (int rc = alloc_logs(c, want)) return rc;
     size_t need = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, need, c->lkey_in.p, c->lkey_out.p, c->lg_val.p, c->lval_out.p, (int)want,
-                                    0, 64, c->stream);
+    cub::DeviceRadixSort::SortPairs(nullptr, need, c->lkey_in.p, c->lkey_out.p, c->lg_val.p, c->lval_out.p,
+                                    (int64_t)want, 0, 64, c->stream);
     if (need > c->cub_tmp.n && c->cub_tmp.alloc(need)) return EMC_E_OOM;
     return 0;
 }
@@ -961,6 +967,7 @@ extern "C" int emc_run_batch(emc_ctx* c, const emc_batch_args* a, emc_batch_resu
     if (!c->configured) return fail_arg("emc_configure first");
     EMC_TRY_CUDA(cudaSetDevice(c->device));
     std::memset(res, 0, sizeof(*res));
+    c->G.guard = c->cfg.box_guard ? 1 : 0;      // box guard extension (emc.h), per run
     int64_t l0 = c->launches;
     int reruns = 0;
     if (int rc = presize_logs(c)) return rc;
@@ -1163,6 +1170,26 @@ extern "C" int emc_xs_lookup(emc_ctx* c, int64_t n, const int32_t* mats, const d
     if (partials) to_host(partials, dp, n * max_comp * 4, st);
     EMC_TRY_CUDA(cudaStreamSynchronize(st));
     dm.release(); de.release(); ds.release(); dp.release();
+    return 0;
+}
+
+extern "C" int emc_grid_index(emc_ctx* c, int64_t n, const int32_t* entry, const double* E, int32_t* out)
+{
+    if (!c || !c->have_lib) return fail_arg("upload a library first");
+    if (n < 0) return fail_arg("emc_grid_index: bad arguments");
+    for (int64_t i = 0; i < n; ++i)
+        if (entry[i] < 0 || entry[i] >= c->n_entries) return fail_arg("unknown composition entry");
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    cudaStream_t st = c->stream;
+    DBuf<int32_t> dk, dout; DBuf<double> de;
+    if (to_dev(dk, entry, n, st) || to_dev(de, E, n, st) || dout.alloc(std::max<int64_t>(1, 2 * n))) return EMC_E_OOM;
+    if (n) {
+        k_api_bracket<<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(c->L, n, dk.p, de.p, dout.p);
+        EMC_CHECK_LAUNCH(c);
+    }
+    to_host(out, dout, 2 * n, st);
+    EMC_TRY_CUDA(cudaStreamSynchronize(st));
+    dk.release(); de.release(); dout.release();
     return 0;
 }
 

@@ -83,8 +83,15 @@ __global__ void __launch_bounds__(128) k_history(BatchP bp, DLib L, DGeom G, DSr
             x = __dadd_rn(x, __dmul_rn(dx, ell));
             y = __dadd_rn(y, __dmul_rn(dy, ell));
             z = __dadd_rn(z, __dmul_rn(dz, ell));
-            bool died = false;
-            if (crossing && G.vacuum && surf >= SURF_XMIN && surf <= SURF_ZMAX) {
+            bool died = false, guarded = false;
+            if (!crossing && G.guard && box_guard(x, y, z, dx, dy, dz, G)) {   // box guard (extension)
+                atomicAdd(cnt + CNT_BOX_GUARD, 1ull);
+                guarded = true;
+                if (G.vacuum) { leaks += 1; died = true; }
+                else kd = locate_point(x, y, z, G, ax, m);
+            }
+            if (guarded) {
+            } else if (crossing && G.vacuum && surf >= SURF_XMIN && surf <= SURF_ZMAX) {
                 leaks += 1; died = true;                 // vacuum boundary (extension)
             } else if (crossing) {
                 if (surf >= SURF_XMIN && surf <= SURF_ZMAX) {
@@ -103,6 +110,11 @@ __global__ void __launch_bounds__(128) k_history(BatchP bp, DLib L, DGeom G, DSr
                     ax = dz > 0.0 ? jpl : jpl - 1;
                 }
                 m = kd == KIND_FUEL ? G.fuel_mats[ax] : G.mod_mat;
+                if (G.guard && box_guard(x, y, z, dx, dy, dz, G)) {
+                    atomicAdd(cnt + CNT_BOX_GUARD, 1ull);
+                    if (G.vacuum) { leaks += 1; died = true; }
+                    else kd = locate_point(x, y, z, G, ax, m);
+                }
             } else {
                 // --- collision (K:814-923)
                 ev_c += 1;

@@ -490,6 +490,16 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
                         to_cross = crossing;
                         leak = crossing && G.vacuum && surf >= SURF_XMIN && surf <= SURF_ZMAX;
                         if (crossing && !leak) cross_surface(a, b, d, G);
+                        if (G.guard && !leak && box_guard(a.x, a.y, a.z, b.dx, b.dy, b.dz, G)) {
+                            atomicAdd(cnt + CNT_BOX_GUARD, 1ull);      // rare: ~1e-9 per history
+                            to_col = false; to_cross = true;           // no collision here: re-look-up
+                            if (G.vacuum) { leak = true; d.surf = SURF_XMIN; }
+                            else {
+                                int32_t ax, mt;
+                                d.kind = (int8_t)locate_point(a.x, a.y, a.z, G, ax, mt);
+                                d.axial = ax; d.mat = mt;
+                            }
+                        }
                         kE = a.E;
                     }
                     p.a = a; p.b = b;

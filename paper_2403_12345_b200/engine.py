@@ -101,7 +101,8 @@ class DeviceEngine:
                              config.max_in_flight, int(config.mode == "history"),
                              int(config.tally_mode == "fused"),
                              int(config.reduction == "deterministic"),
-                             int(bool(config.sort_enabled)), int(config.sort_every_n), 0,
+                             int(bool(config.sort_enabled)), int(config.sort_every_n),
+                             int(bool(getattr(config, "box_guard", False))),
                              config.seed & ((1 << 63) - 1), config.alpha_scatter,
                              config.fission_temperature, int(config.perturb_particle))
         N.check(self.lib.emc_configure(self._h, C.byref(cfg)), "emc_configure")
@@ -191,6 +192,15 @@ class DeviceEngine:
         if parts is not None and self.max_comp == 0:
             parts = parts[:, :0]
         return sums, parts
+
+    def grid_index(self, entries: np.ndarray, ens: np.ndarray) -> np.ndarray:
+        """[n, 2] (clamp state, bracket index) of composition entries at E."""
+        entries = np.ascontiguousarray(entries, np.int32)
+        ens = np.ascontiguousarray(ens, np.float64)
+        out = np.zeros((entries.shape[0], 2), np.int32)
+        N.check(self.lib.emc_grid_index(self._h, entries.shape[0], N.ptr(entries), N.ptr(ens), N.ptr(out)),
+                "emc_grid_index")
+        return out
 
     def locate(self, pos: np.ndarray) -> np.ndarray:
         out = np.zeros((pos.shape[0], 3), np.int32)

@@ -45,6 +45,7 @@ _COUNTER_SUMS = (("captures", 5), ("fissions", 6), ("sourced", 7), ("energy_clam
 _COUNTER_MAXES = (("max_draws_per_history", 8), ("max_log_entries_per_history", 20),
                   ("max_in_flight_observed", 19))
 _COUNTER_LEAKS = (("leaks", 22),)          # extension: vacuum boundaries
+_COUNTER_GUARD = (("box_guard", 23),)      # extension: RunConfig.box_guard
 
 _ENGINES: dict[int, DeviceEngine] = {}
 
@@ -155,7 +156,8 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
         if sourced != ppb or deaths != ppb:
             raise EventMCError(f"neutron bookkeeping broken in batch {b}: {sourced} sourced, "
                                f"{deaths} absorbed or leaked, {ppb} expected")
-        sums_spec = _COUNTER_SUMS + (_COUNTER_LEAKS if pincell.boundary == "vacuum" else ())
+        sums_spec = _COUNTER_SUMS + (_COUNTER_LEAKS if pincell.boundary == "vacuum" else ()) + \
+            (_COUNTER_GUARD if config.box_guard else ())
         batch_counters = combine_counters(per_rank, sums_spec, _COUNTER_MAXES)
         for name, _ in sums_spec:
             run_counters[name] = run_counters.get(name, 0) + batch_counters[name]

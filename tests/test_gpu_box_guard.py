@@ -1,0 +1,96 @@
+"""Box guard on the B200 (RunConfig.box_guard, include/emc.h) and the bench's
+exact C4 configuration run for the driver's 5 + 20 batches.
+
+The escape history (tests/golden/c4_escape.json; see tests/test_box_guard.py)
+is replayed on the device alone: the engine is configured for the single
+particle index gid of a 40M-particle batch and sourced from a one-site bank
+holding the history's recorded source site, so it draws the same stream.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2403_12345_b200")
+
+
+@pytest.fixture(scope="module")
+def escape():
+    with open(os.path.join(GOLDEN, "c4_escape.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.fixture(scope="module")
+def c4():
+    return P.depleted_pincell(272, 3, 11303, 100, seed=1)
+
+
+def _device_history(escape, c4, guard):
+    import torch
+    from paper_2403_12345_b200.engine import DeviceEngine
+    lib, cell = c4
+    eng = DeviceEngine(0)
+    eng.upload_library(lib)
+    eng.upload_geometry(cell)
+    cfg = P.RunConfig(particles_per_batch=escape["ppb"], inactive_batches=0, active_batches=22,
+                      mode="event", max_in_flight=1, reduction="fast", seed=escape["seed"],
+                      box_guard=bool(guard))
+    eng.set_extensions(cell, cfg)
+    eng.configure(cfg, escape["gid"], 1)
+    src = [torch.tensor([float.fromhex(h)], dtype=torch.float64, device="cuda")
+           for h in escape["source_site_hex"]]
+    eng.set_source_device([t.data_ptr() for t in src], 1, 0.5, keep=src)
+    out = eng.run_batch(escape["batch"], float.fromhex(escape["k_run_hex"]), batch0=False, score=True)
+    torch.cuda.synchronize()
+    cols = eng.bank_to_host()
+    eng.close()
+    sites = [[float(cols[k][j]).hex() for k in range(2, 9)] for j in range(cols[0].shape[0])]
+    return out, sites
+
+
+@pytest.mark.parametrize("guard", [0, 1])
+def test_escape_history_matches_oracle(escape, c4, guard):
+    out, sites = _device_history(escape, c4, guard)
+    want = escape[f"guard{guard}"]
+    assert out.error == 0
+    assert sites == want["sites_hex"]
+    assert int(out.counters[23]) == want["counters"]["box_guard"]
+    for k, i in (("events_lookup", 12), ("events_advance", 13), ("events_collision", 14),
+                 ("fissions", 6), ("captures", 5)):
+        assert int(out.counters[i]) == want["counters"][k], k
+
+
+@pytest.mark.parametrize("name", ["c1_event", "preset251_event_w2"])
+def test_guard_keeps_reference_fingerprint(golden, name):
+    from conftest import golden_library
+    run = golden["runs"][name]
+    pm = golden["problems"][run["problem"]]
+    cell = P.Pincell(n_axial=pm["n_axial"], fuel_material_ids=pm["fuel_material_ids"],
+                     moderator_material_id=pm["moderator_material_id"])
+    res = P.run_replicated(P.RunConfig(**dict(run["config"], box_guard=True)),
+                           golden_library(run["problem"]), cell)
+    assert res.physics_fingerprint() == run["fingerprint"]
+    assert res.counters["box_guard"] == 0
+
+
+@pytest.mark.slow
+def test_bench_c4_configuration_completes_driver_batches():
+    """bench.py's C4 workload exactly as the driver runs it (--steps 20
+    --warmup 5): 40M particles x 25 batches, seed 42, fast reduction, box
+    guard on.  Without the guard this configuration stops in batch 22."""
+    import bench
+    wl = bench.WORKLOAD
+    lib, cell = P.depleted_pincell(272, 3, 11303, 100, seed=1)
+    cfg = P.RunConfig(particles_per_batch=wl["ppb_per_gpu"], inactive_batches=5, active_batches=20,
+                      mode="event", sort_enabled=True, max_in_flight=wl["ppb_per_gpu"],
+                      tally_mode="fused", reduction=wl["reduction"], seed=wl["seed"], box_guard=True)
+    res = P.run_event(cfg, lib, cell)
+    assert res.counters["sourced"] == 25 * wl["ppb_per_gpu"]
+    assert res.counters["box_guard"] >= 1          # the batch-21 escape (and any others) guarded
+    assert 0.5 < res.k_mean < 1.5 and res.k_stderr < 1e-3
