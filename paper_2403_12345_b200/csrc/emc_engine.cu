@@ -114,7 +114,7 @@ struct emc_ctx {
     DBuf<int32_t> mat_group, grp_off; DBuf<NucRef> gnuc; DBuf<DD> ddT; DBuf<double> denS; DBuf<IvRec> iv; DBuf<int32_t> nsafe;
     int32_t n_groups = 0;
     DLib L{};
-    int32_t n_materials = 0, max_comp = 0;
+    int32_t n_materials = 0, max_comp = 0, n_entries = 0;
     double nu_max = 0.0;         // largest nu of the library (bounds the fission-site ordinal)
     int64_t lib_bytes = 0;
 
@@ -412,6 +412,7 @@ extern "C" int emc_upload_library(emc_ctx* c, const emc_library* lib)
     EMC_TRY_CUDA(lk_set_smem(c->lk_smem));
     if (const char* lc = getenv("EMC_LK_CFG")) c->lk_cfg = std::max(0, std::min(LK_NCFG - 1, atoi(lc)));
     c->n_materials = (int32_t)nm;
+    c->n_entries = (int32_t)ne;
     c->max_comp = maxc;
     c->nu_max = 0.0;
     for (int64_t i = 0; i < nn; ++i) c->nu_max = std::max(c->nu_max, lib->nu[i]);

@@ -19,6 +19,13 @@
  * 2*pi*u in [0, 2*pi)).  Larger sin/cos arguments need glibc's __branred and
  * are not used anywhere on the transport path (they return NaN here).
  *
+ * Licence note: derived from the GNU C Library 2.39 (sysdeps/ieee754/dbl-64
+ * e_log.c / s_sin.c, FMA builds), which is Copyright (C) the Free Software
+ * Foundation and contributors and licensed under the GNU Lesser General Public
+ * License v2.1 or later.  This file and the generated emc_glibc_tables.h are
+ * a derivative work of that code and are distributed under the same LGPL-2.1+
+ * terms; the rest of this repository is not derived from glibc.
+ *
  * Validated against the system libm by tests/test_libm_replica.py (host build,
  * ~10^8 samples of the transport argument distributions, 0 mismatches
  * required) and on the GPU by tests/test_gpu_parity.py.

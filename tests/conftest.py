@@ -59,3 +59,23 @@ def gpu_available():
         return _native.device_count() > 0
     except Exception:  # noqa: BLE001
         return False
+
+
+@pytest.fixture
+def engine_env(monkeypatch):
+    """Set EMC_* tuning variables for one test: the engine reads them when it
+    is created, so the cached per-device engines are dropped before and after."""
+    def _drop():
+        from paper_2403_12345_b200 import replication
+        for eng in list(replication._ENGINES.values()):
+            eng.close()
+        replication._ENGINES.clear()
+
+    def _set(**env):
+        for k, v in env.items():
+            monkeypatch.setenv(k, str(v))
+        _drop()
+
+    yield _set
+    monkeypatch.undo()
+    _drop()
