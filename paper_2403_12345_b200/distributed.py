@@ -19,6 +19,13 @@ rank-local canonical banks).  Per batch:
     (the reference's `sums += w.wbins` in worker order, R:238-240);
   * counters: all-gather, sums and maxima on the host.
 
+The same collectives also run between threads of ONE process driving several
+GPUs (``ThreadGroup``: the reference's single-process API, where
+``RunConfig.workers`` is a worker-thread count, R:155-190): each thread owns
+one device and one particle block, small arrays are exchanged through shared
+host memory behind a barrier, and bank windows move device to device with
+peer copies (NVLink) -- no NCCL communicator needed.
+
 Everything here is plumbing on torch tensors; the transport arithmetic stays
 in libemc.  The functions take/return plain numpy or torch tensors so the
 host logic is testable with the gloo backend on CPU (tests/test_distributed.py).
@@ -26,22 +33,56 @@ host logic is testable with the gloo backend on CPU (tests/test_distributed.py).
 
 from __future__ import annotations
 
+import threading
 from dataclasses import dataclass
 
 import numpy as np
+
+
+class ThreadGroup:
+    """Collectives between the threads of one process (one thread per GPU).
+
+    Every collective is a rendezvous on one barrier; a thread that fails
+    aborts the barrier so its peers raise BrokenBarrierError instead of
+    waiting forever (run_replicated re-raises the original error)."""
+
+    def __init__(self, size: int):
+        self.size = size
+        self.barrier = threading.Barrier(size)
+        self.slots: list = [None] * size
+        self.shared = None
+
+    def wait(self) -> None:
+        self.barrier.wait()
+
+    def abort(self) -> None:
+        self.barrier.abort()
+
+    def allgather(self, rank: int, obj) -> list:
+        self.slots[rank] = obj
+        self.wait()
+        out = list(self.slots)
+        self.wait()                 # nobody overwrites a slot before all have read it
+        return out
 
 
 @dataclass(frozen=True)
 class World:
     rank: int = 0
     size: int = 1
-    device_backend: bool = False        # True: NCCL (tensors must be on CUDA)
+    device_backend: bool = False        # True: collectives on CUDA tensors (NCCL, or peer copies)
 
     forced: bool = False                # EMC_FORCE_COLLECTIVES=1: collectives even at size 1
+    group: ThreadGroup | None = None    # set: threads of one process, not torch.distributed
+    device: int = 0                     # this rank's GPU (thread worlds)
 
     @property
     def distributed(self) -> bool:
         return self.size > 1 or self.forced
+
+    @property
+    def threads(self) -> bool:
+        return self.group is not None
 
 
 def current_world() -> World:
@@ -63,6 +104,8 @@ def block_of(rank: int, size: int, ppb: int) -> tuple[int, int]:
 
 def _tensor_device(world: World):
     import torch
+    if world.threads:
+        return torch.device("cuda", world.device) if world.device_backend else torch.device("cpu")
     return torch.device("cuda", torch.cuda.current_device()) if world.device_backend \
         else torch.device("cpu")
 
@@ -71,6 +114,8 @@ def allgather_array(world: World, arr: np.ndarray) -> np.ndarray:
     """Stack a small same-shape numpy array from every rank: [W, ...]."""
     if not world.distributed:
         return arr[None, ...].copy()
+    if world.threads:
+        return np.stack(world.group.allgather(world.rank, np.array(arr, copy=True)))
     import torch
     import torch.distributed as dist
     t = torch.as_tensor(np.ascontiguousarray(arr)).to(_tensor_device(world))
@@ -104,6 +149,15 @@ def chained_fold(world: World, fold_local, n_bins: int) -> np.ndarray:
     `fold_local(init: np.ndarray | None) -> np.ndarray`."""
     if not world.distributed:
         return fold_local(None)
+    if world.threads:
+        g = world.group
+        for r in range(world.size):          # the chain: one rank folds at a time, in order
+            if world.rank == r:
+                g.shared = fold_local(None if r == 0 else g.shared)
+            g.wait()
+        final = np.array(g.shared, copy=True)
+        g.wait()
+        return final
     import torch
     import torch.distributed as dist
     dev = _tensor_device(world)
@@ -125,28 +179,36 @@ BANK_DTYPES = ("int64", "int32") + ("float64",) * 7
 
 
 def gather_bank(world: World, local_cols, counts: np.ndarray):
-    """All-gather rank banks into the global canonical bank.
+    """Gather the rank banks into the global canonical bank on rank 0 only
+    (the run's single full-bank movement, after the last batch).
 
     `local_cols`: 9 torch tensors (parent, ordinal, x..energy) of this rank's
-    canonical bank; `counts`: int64[W] site counts.  Returns 9 torch tensors
-    of length sum(counts), rank order, on the collective's device."""
+    canonical bank; `counts`: int64[W] site counts.  Returns, on rank 0, 9
+    HOST torch tensors of length sum(counts) in rank order; None elsewhere."""
     import torch
-    import torch.distributed as dist
     total = int(counts.sum())
     if not world.distributed:
-        return [c[:total] for c in local_cols]
+        return [c[:total].cpu() for c in local_cols]
+    n = int(counts[world.rank])
+    if world.threads:
+        parts = world.group.allgather(world.rank, [c[:n] for c in local_cols])
+        if world.rank != 0:
+            return None
+        return [torch.cat([parts[r][k].cpu() for r in range(world.size)])
+                for k in range(len(local_cols))]
+    import torch.distributed as dist
     mx = int(counts.max())
     dev = _tensor_device(world)
     out = []
     for col in local_cols:
         padded = torch.zeros(max(mx, 1), dtype=col.dtype, device=dev)
-        n = int(counts[world.rank])
         if n:
             padded[:n] = col[:n].to(dev)
-        parts = [torch.empty_like(padded) for _ in range(world.size)]
-        dist.all_gather(parts, padded)
-        out.append(torch.cat([parts[r][:int(counts[r])] for r in range(world.size)]))
-    return out
+        parts = [torch.empty_like(padded) for _ in range(world.size)] if world.rank == 0 else None
+        dist.gather(padded, parts, dst=0)
+        if world.rank == 0:
+            out.append(torch.cat([parts[r][:int(counts[r])].cpu() for r in range(world.size)]))
+    return out if world.rank == 0 else None
 
 
 def device_view(ptr: int, n: int, dtype: str, device: int):
@@ -219,6 +281,8 @@ def exchange_bank(world: World, local_cols, counts: np.ndarray, ppb: int, u: flo
         return out
 
     me = world.rank
+    if world.threads:
+        return _exchange_threads(world, local_cols, offs, wins, n), wins[me][0]
     send_plan = [pieces(q, me) for q in range(world.size)]
     recv_plan = [pieces(me, r) for r in range(world.size)]
     send_splits = [sum(b - a for a, b in pl) for pl in send_plan]
@@ -253,3 +317,48 @@ def exchange_bank(world: World, local_cols, counts: np.ndarray, ppb: int, u: flo
             win[d:d + (b - a)] = recv[p:p + (b - a)]
         out_cols.append(win)
     return out_cols, wins[me][0]
+
+
+def _exchange_threads(world: World, local_cols, offs: np.ndarray, wins, n: int):
+    """Thread-world bank exchange: every thread publishes its bank columns
+    (tensors on its own GPU) and copies the pieces of its window straight from
+    the owners' memory (device-to-device peer copies over NVLink), then waits
+    until every thread has finished reading before anyone's next batch may
+    overwrite its bank."""
+    import torch
+    dev = _tensor_device(world)
+    parts = world.group.allgather(world.rank, list(local_cols))
+    out = []
+    for k in range(len(local_cols)):
+        pieces = []
+        for a, b in _segments(*wins[world.rank], n):
+            for r in range(world.size):
+                lo_, hi_ = max(a, int(offs[r])), min(b, int(offs[r + 1]))
+                if hi_ > lo_:
+                    src = parts[r][k][lo_ - int(offs[r]):hi_ - int(offs[r])]
+                    pieces.append(src.to(dev, non_blocking=False))
+        out.append(torch.cat(pieces) if pieces else local_cols[k][:0].to(dev))
+    if dev.type == "cuda":
+        torch.cuda.synchronize(dev)
+    world.group.wait()
+    return out
+
+
+def allreduce_tensor(world: World, x):
+    """Sum of a tensor over ranks (mesh tallies), rank order for threads."""
+    if not world.distributed:
+        return x
+    if world.threads:
+        parts = world.group.allgather(world.rank, x)
+        tot = parts[0].to(x.device).clone()
+        for r in range(1, world.size):
+            tot += parts[r].to(x.device)
+        world.group.wait()           # peers keep their buffers until everyone has summed
+        return tot
+    import torch.distributed as dist
+    if world.device_backend:
+        dist.all_reduce(x)
+        return x
+    h = x.cpu()                      # gloo (tests): through host memory
+    dist.all_reduce(h)
+    return h.to(x.device)

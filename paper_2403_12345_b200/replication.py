@@ -6,9 +6,15 @@ Per batch (R:198-286): run this rank's particle block on its GPU
 codes to exceptions (R:214-219), gather the bank and reduce tallies across
 ranks (distributed.py), compute k (R:243-249), check neutron bookkeeping
 (R:250-257), accumulate counters (R:259-269) and resample the next source
-from the global canonical bank (R:271-280).  In a single process the GPU is
-the whole worker pool: ``config.workers`` is validated but all particles run
-on device 0; under torch.distributed each rank drives its own GPU.
+from the global canonical bank (R:271-280).
+
+Ranks and GPUs.  Under torch.distributed (torchrun, one process per GPU)
+each rank drives its own GPU.  In a single process ``config.workers = W``
+(the reference's worker-thread count) drives min(W, visible GPUs) devices,
+one host thread per device, with the collectives of distributed.ThreadGroup
+(peer copies for the bank windows); physics is worker-invariant (the
+reference's acceptance criterion 2), so W beyond the GPU count only changes
+the assignment, never the result.
 """
 
 from __future__ import annotations
@@ -19,9 +25,9 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 from . import prng, xslib
-from .distributed import (BANK_DTYPES, World, allgather_array, block_of, chained_fold,
-                          combine_counters, current_world, device_view, exchange_bank, fast_bins,
-                          gather_bank)
+from .distributed import (BANK_DTYPES, ThreadGroup, World, allgather_array, allreduce_tensor,
+                          block_of, chained_fold, combine_counters, current_world, device_view,
+                          exchange_bank, gather_bank)
 from .engine import DeviceEngine
 from .errors import (ConfigurationError, EventMCError, GeometryError, PhysicsError,
                      PopulationCollapseError, RunawayHistoryError, StreamOverlapError)
@@ -47,14 +53,15 @@ _COUNTER_MAXES = (("max_draws_per_history", 8), ("max_log_entries_per_history", 
 _COUNTER_LEAKS = (("leaks", 22),)          # extension: vacuum boundaries
 _COUNTER_GUARD = (("box_guard", 23),)      # extension: RunConfig.box_guard
 
-_ENGINES: dict[int, DeviceEngine] = {}
+_ENGINES: dict[tuple[int, int], DeviceEngine] = {}
 
 
-def engine_for(device: int, library, pincell) -> DeviceEngine:
-    """Per-device engine reused across runs; re-uploads changed inputs only."""
-    eng = _ENGINES.get(device)
+def engine_for(device: int, library, pincell, slot: int = 0) -> DeviceEngine:
+    """Per-(device, slot) engine reused across runs; re-uploads changed
+    inputs only.  `slot` > 0 only when several ranks share one GPU (tests)."""
+    eng = _ENGINES.get((device, slot))
     if eng is None:
-        eng = _ENGINES[device] = DeviceEngine(device)
+        eng = _ENGINES[(device, slot)] = DeviceEngine(device)
     if eng.library_obj is None or eng.library_obj() is not library:
         eng.upload_library(library)
     if eng.pincell_obj is None or eng.pincell_obj() is not pincell:
@@ -63,20 +70,47 @@ def engine_for(device: int, library, pincell) -> DeviceEngine:
 
 
 def _local_device(world: World) -> int:
+    if world.threads:
+        return world.device
     if not world.distributed:
         return 0
     import torch
     return torch.cuda.current_device() if world.device_backend else 0
 
 
-def run_replicated(config: RunConfig, library, pincell, index=None, *,
-                   on_batch=None) -> RunResult:
-    """Run the configured k-eigenvalue problem on this process's GPU(s).
+def _device_count() -> int:
+    from . import _native
+    try:
+        return _native.device_count()
+    except Exception:  # noqa: BLE001
+        return 0
 
+
+def resolve_devices(config: RunConfig, devices=None) -> list[int]:
+    """GPUs a single-process run drives: `devices` if given (a device may be
+    listed twice: several ranks on one GPU, for tests), else the first
+    min(config.workers, visible GPUs)."""
+    if devices is not None:
+        devices = [int(d) for d in devices]
+        if not devices:
+            raise ConfigurationError("devices must not be empty")
+        if len(devices) > config.particles_per_batch:
+            raise ConfigurationError("more devices than particles per batch")
+        return devices
+    n = _device_count()
+    return list(range(max(1, min(config.workers, n))))
+
+
+def run_replicated(config: RunConfig, library, pincell, index=None, *,
+                   on_batch=None, devices=None) -> RunResult:
+    """Run the configured k-eigenvalue (or fixed-source) problem.
+
+    Under torch.distributed: this rank's block on this process's GPU.
+    Otherwise: ``resolve_devices(config, devices)`` GPUs, one thread each.
     ``on_batch(b, phase, engine)`` (phase 'start'/'end') is an optional
-    instrumentation hook (bench.py records CUDA events through it)."""
+    instrumentation hook (bench.py records CUDA events through it; rank 0's
+    engine only)."""
     config.validate()
-    ppb = config.particles_per_batch
     for mid in list(pincell.fuel_material_ids) + [pincell.moderator_material_id]:
         if mid < 0 or mid >= library.n_materials:
             raise ConfigurationError(f"geometry references material {mid} "
@@ -86,10 +120,62 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
         xslib.merge_channels(library, index)   # API parity (R:145-152); device search is log-hashed
 
     world = current_world()
+    if world.distributed:
+        if devices is not None:
+            raise ConfigurationError("devices= is for single-process runs; under "
+                                     "torch.distributed each rank uses its own GPU")
+        return _run_rank(config, library, pincell, world, on_batch)
+    devs = resolve_devices(config, devices)
+    if len(devs) == 1:
+        return _run_rank(config, library, pincell, World(device=devs[0]), on_batch)
+    return _run_threads(config, library, pincell, devs, on_batch)
+
+
+def _run_threads(config, library, pincell, devs, on_batch) -> RunResult:
+    import threading
+
+    import torch
+    torch.cuda.init()                           # once, before the device threads start
+    group = ThreadGroup(len(devs))
+    results: list = [None] * len(devs)
+    errors: list = [None] * len(devs)
+    seen: dict[int, int] = {}
+    slots = []
+    for d in devs:
+        slots.append(seen.get(d, 0))
+        seen[d] = seen.get(d, 0) + 1
+
+    def body(r):
+        try:
+            torch.cuda.set_device(devs[r])
+            w = World(rank=r, size=len(devs), device_backend=True, group=group, device=devs[r])
+            results[r] = _run_rank(config, library, pincell, w, on_batch if r == 0 else None,
+                                   slot=slots[r])
+        except BaseException as e:  # noqa: BLE001
+            errors[r] = e
+            group.abort()
+
+    threads = [threading.Thread(target=body, args=(r,), name=f"emc-rank{r}") for r in range(len(devs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    real = [e for e in errors if e is not None and not isinstance(e, threading.BrokenBarrierError)]
+    if real:
+        raise real[0]
+    if any(e is not None for e in errors):
+        raise errors[0]
+    return results[0]
+
+
+def _run_rank(config: RunConfig, library, pincell, world: World, on_batch, slot: int = 0) -> RunResult:
+    """One rank's share of run_replicated; the returned RunResult is complete
+    on rank 0 (global k, tallies, counters, final bank)."""
+    ppb = config.particles_per_batch
     if world.distributed and world.size > ppb:
         raise ConfigurationError("more ranks than particles per batch")
     g_lo, g_hi = block_of(world.rank, world.size, ppb)
-    eng = engine_for(_local_device(world), library, pincell)
+    eng = engine_for(_local_device(world), library, pincell, slot)
     eng.set_extensions(pincell, config)
     eng.configure(config, g_lo, g_hi - g_lo)
     fixed_source = config.run_mode == "fixed_source"
@@ -119,16 +205,28 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
         t_batch = time.perf_counter()
         out = eng.run_batch(b, k_run, batch0=(b == 0), score=active)
         launches += out.launches
-        errs = allgather_array(world, np.array([out.error, out.error_gid], np.int64))
-        for code, gid in errs:
+        # ONE small all-gather per batch carries every per-rank scalar:
+        # error, site count, iterations, the 24 counters, the 4 timings (as
+        # bit patterns) and, in fast mode, the tally bins (bit patterns)
+        t0 = time.perf_counter()
+        fast = None if use_logs else eng.reduce_bins(None)
+        pack = np.concatenate([np.array([out.error, out.error_gid, out.n_sites, out.iterations], np.int64),
+                               np.asarray(out.counters, np.int64),
+                               np.ascontiguousarray(out.timings, np.float64).view(np.int64)] +
+                              ([np.ascontiguousarray(fast, np.float64).view(np.int64)] if fast is not None else []))
+        allp = allgather_array(world, pack)
+        nc = out.counters.shape[0]
+        nt = out.timings.shape[0]
+        per_rank = allp[:, 4:4 + nc]
+        tim_rank = np.ascontiguousarray(allp[:, 4 + nc:4 + nc + nt]).view(np.float64)
+        for code, gid in allp[:, :2]:
             if code:
                 cls, msg = _ERRORS[int(code)]
                 raise cls(f"{msg} (batch {b}, particle {int(gid)})")
 
         # fission bank: global canonical order = rank-ordered concatenation;
         # each rank receives only the window its next batch resamples from
-        t0 = time.perf_counter()
-        counts = allgather_array(world, np.array([out.n_sites], np.int64))[:, 0]
+        counts = allp[:, 2].copy()
         n_bank = int(counts.sum())
         local = None
         if world.distributed:
@@ -136,21 +234,21 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
                      for p, dt in zip(eng.bank_device_ptrs(), BANK_DTYPES)] \
                 if world.device_backend else \
                 [__import__("torch").as_tensor(c) for c in eng.bank_to_host()]
-        timings["merge"] += time.perf_counter() - t0
 
         # tallies + k
-        t0 = time.perf_counter()
         if use_logs:
             sums = chained_fold(world, lambda init: eng.reduce_bins(init), layout.n_bins)
         else:
-            sums = fast_bins(world, eng.reduce_bins(None))
+            bins_rank = np.ascontiguousarray(allp[:, 4 + nc + nt:]).view(np.float64)
+            sums = np.zeros(layout.n_bins)
+            for r in range(bins_rank.shape[0]):       # rank order (R:238-240)
+                sums += bins_rank[r]
         timings["reduce"] += time.perf_counter() - t0
         batch_sums[b] = sums
         keff_values[b] = sums[layout.keff_bin] / weight
 
         if mesh is not None and active:
             mesh.add_batch()
-        per_rank = allgather_array(world, out.counters)
         sourced = int(per_rank[:, 7].sum())
         deaths = int(per_rank[:, 5].sum() + per_rank[:, 6].sum() + per_rank[:, 22].sum())
         if sourced != ppb or deaths != ppb:
@@ -165,14 +263,13 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
             run_counters[name] = max(run_counters.get(name, 0), batch_counters[name])
         if active:
             nuclide_lookups_active += int(per_rank[:, 21].sum())
-            act["lookup_active_s"] += float(allgather_array(world, out.timings)[:, 0].sum())
-            act["lookup_launches_active"] += int(allgather_array(
-                world, np.array([out.iterations], np.int64)).sum())
+            act["lookup_active_s"] += float(tim_rank[:, 0].sum())
+            act["lookup_launches_active"] += int(allp[:, 3].sum())
             # host<->device traffic of the batch: control block per iteration,
             # counters + tally bins at the end (engine.py / emc_engine.cu)
             act["h2d_bytes_active"] += 48 + 64
             act["d2h_bytes_active"] += 48 * (out.iterations + 2) + 24 * 8 + layout.n_bins * 8
-        tim = allgather_array(world, out.timings).sum(axis=0)
+        tim = tim_rank.sum(axis=0)
         for key, i in (("lookup", 0), ("advance", 1), ("collision", 2), ("sort", 3)):
             timings[key] += float(tim[i])
 
@@ -204,14 +301,18 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
         else:
             inactive_wall += wall
 
-    # final canonical bank on the host: the run's only full all-gather (every
-    # batch before moved just the resampling windows)
+    # final canonical bank on rank 0's host: the run's only full-bank movement
+    # (every batch before moved just the resampling windows)
     if world.distributed:
-        cols = [c.cpu().numpy() for c in gather_bank(world, last_local, last_counts)]
+        g = gather_bank(world, last_local, last_counts)
+        cols = [c.numpy() for c in g] if g is not None else \
+            [np.empty(0, dt) for dt in BANK_DTYPES]
     else:
         cols = list(eng.bank_to_host())
     bank = FissionBank(*cols)
     act["d2h_bytes_final_bank"] = 68 * len(bank)      # after the loop: not inside the active wall
+    act["ranks"] = world.size
+    act["devices"] = world.size if (world.threads or world.device_backend) else 1
 
     keff = KeffSeries(keff_values, config.inactive_batches)
     k_mean = k_stderr = tally_mean = tally_stderr = None
@@ -257,15 +358,7 @@ class _MeshAccumulator:
 
     def add_batch(self):
         import torch
-        x = self.view.clone()
-        if self.world.distributed:
-            import torch.distributed as dist
-            if self.world.device_backend:
-                dist.all_reduce(x)
-            else:                                       # gloo (tests): through host memory
-                h = x.cpu()
-                dist.all_reduce(h)
-                x = h.to(x.device)
+        x = allreduce_tensor(self.world, self.view.clone())
         self.sum += x
         self.sq += x * x
         torch.cuda.synchronize(x.device)     # the next batch re-zeroes the buffer on the engine stream
@@ -301,9 +394,16 @@ class ScalingRow:
 def weak_scaling_study(base_config: RunConfig, library, pincell, worker_list: list[int],
                        particles_per_worker: int, index=None) -> list[ScalingRow]:
     """particles_per_batch = W * particles_per_worker; efficiency =
-    active_rate(W) / (W * active_rate(1)) (R:329-355)."""
+    active_rate(W) / (W * active_rate(1)) (R:329-355).  Row W runs on W GPUs
+    (one thread per device, run_replicated); a W larger than the visible GPU
+    count would measure one GPU's throughput under a W-GPU label, so it is
+    refused."""
     if not worker_list or worker_list[0] != 1 or sorted(worker_list) != list(worker_list):
         raise ConfigurationError("worker list must be ascending and start at 1")
+    ndev = _device_count()
+    if worker_list[-1] > ndev:
+        raise ConfigurationError(f"scaling study over {worker_list[-1]} workers needs "
+                                 f"{worker_list[-1]} GPUs; {ndev} visible")
     if base_config.active_batches < 1 or base_config.inactive_batches < 1:
         raise ConfigurationError("scaling study needs at least one batch in each phase")
     rows: list[ScalingRow] = []

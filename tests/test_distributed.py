@@ -59,8 +59,8 @@ def _worker(rank, world, port, q):
         cols = [torch.arange(lo, lo + n, dtype=torch.int64), torch.zeros(n, dtype=torch.int32)] + \
             [torch.full((n,), float(rank)) for _ in range(7)]
         g = D.gather_bank(w, cols, counts)
-        ok_bank = g[0].tolist() == list(range(int(counts.sum()))) and \
-            g[2].tolist() == [0.0] * 3 + [1.0] * 5
+        ok_bank = (g[0].tolist() == list(range(int(counts.sum()))) and
+                   g[2].tolist() == [0.0] * 3 + [1.0] * 5) if rank == 0 else g is None
 
         per_rank = D.allgather_array(w, np.array([rank + 1, 10 * (rank + 1)], np.int64))
         comb = D.combine_counters(per_rank, (("s", 0),), (("m", 1),))
@@ -156,3 +156,47 @@ def test_needed_window_covers_resample_indices():
             # tight: ~(block size) x n/ppb sites, i.e. ~1/W of the bank
             bound = (hi - lo) * n // ppb + 2 if n >= ppb else min(n, hi - lo)
             assert ln <= bound
+
+
+def _xchg_worker_vec(rank, world, port, q, counts, ppb, u):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = D.current_world()
+        counts = np.asarray(counts, np.int64)
+        n = int(counts.sum())
+        lo = int(counts[:rank].sum())
+        glob = np.arange(n, dtype=np.float64) * 1.5 + 0.25
+        mine = [torch.from_numpy(glob[lo:lo + int(counts[rank])].copy())]
+        win, wlo = D.exchange_bank(w, mine, counts, ppb, u)
+        g_lo, g_hi = D.block_of(rank, world, ppb)
+        g = np.arange(g_lo, g_hi, dtype=np.float64)
+        i = np.clip(np.floor(((g + u) * float(n)) / float(ppb)), 0, n - 1).astype(np.int64) \
+            if n >= ppb else (g % n).astype(np.int64)
+        j = (i - wlo) % n
+        ok = bool((j < win[0].shape[0]).all()) and np.array_equal(win[0].numpy()[j], glob[i])
+        q.put((rank, ok, int(win[0].shape[0])))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world8_exchange_c4_like():
+    """Eight gloo ranks at C4's shape scaled down 100x (400k particles per
+    rank, ~1 site per particle, uneven counts): every rank's window holds the
+    sites it resamples, and each moves ~1/8 of the bank, not all of it."""
+    rng = np.random.default_rng(8)
+    counts = rng.integers(380_000, 420_000, 8).tolist()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_xchg_worker_vec, args=(r, 8, port, q, counts, 8 * 400_000, 0.618))
+             for r in range(8)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(8))
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert all(ok for _, ok, _ in res), res
+    assert max(ln for _, _, ln in res) < sum(counts) // 8 + 2
