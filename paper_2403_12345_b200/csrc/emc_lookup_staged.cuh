@@ -63,9 +63,25 @@ struct __align__(128) LkShared {
     unsigned long long full[LK_D], empty[LK_D];
     int32_t grp, bmin, bmax, pad;
     uint32_t word[LK_D][LK_G];
+    uint32_t sfast[LK_D];          // pipelined kernel: every nuclide of the stage takes the fast path
+    uint32_t pad2[(4 - LK_D % 4) % 4];
+    longlong2 hdr[LK_D][LK_G];     // pipelined kernel, fast nuclides: bit patterns of E0[lo+1], E0[lo+2]
     LkMeta meta[LK_D][LK_G];
     IvRec iv[LK_D][LK_G][LK_R];
 };
+
+// A nuclide whose chunk window is staged, at most 3 intervals wide and at
+// least one record away from both grid ends takes the pipelined kernel's fast
+// path: the producer then copies exactly 4 records (lo..lo+3, all inside the
+// grid) and publishes E0[lo+1], E0[lo+2] in the stage header.  Every chunk
+// energy E has its bracket i in [lo, lo+cnt-2] and E < E0[i+1]; records past
+// the window are real grid records with larger energies, so
+//   li = [E0[lo+1] <= E] + [E0[lo+2] <= E]
+// is exactly i - lo with no clamp, and neither end clamp (K:600-612) can apply.
+__host__ __device__ constexpr bool lk_fast(int32_t mode, int32_t cnt, int32_t lo, int32_t last)
+{
+    return mode == LK_STAGED && cnt <= 4 && lo >= 1 && lo + 3 < last;
+}
 
 // density block of one stage: [n_mat][LK_DS] doubles
 __host__ __device__ constexpr size_t lk_den_block(int n_mat) { return (size_t)n_mat * LK_DS * sizeof(double); }
@@ -244,12 +260,16 @@ __device__ __forceinline__ void lk_micro_slow(const DLib& L, const LkMeta& mt, u
 struct LkNext {
     LkMeta mt;
     bool valid;
+    bool fast;                     // lk_fast (pipelined kernel only)
+    long long a1, a2;              // E0[lo+1], E0[lo+2] bit patterns when fast
 };
 
+template <bool HDR = false>
 __device__ __forceinline__ void lk_prefetch(const DLib& L, int32_t e0, int32_t k, int32_t ncomp, int32_t bmin,
                                             int32_t bmax, LkNext& nx)
 {
     nx.valid = k < ncomp;
+    nx.fast = false;
     if (!nx.valid) return;
     const NucRef r = L.gnuc[e0 + k];
     LkMeta& mt = nx.mt;
@@ -264,6 +284,11 @@ __device__ __forceinline__ void lk_prefetch(const DLib& L, int32_t e0, int32_t k
         mt.lo = lo;
         mt.cnt = hi - lo + 2;            // intervals lo..hi plus record hi+1 (<= last)
         mt.mode = mt.cnt <= LK_R ? LK_STAGED : LK_GLOBAL;
+        if (HDR && lk_fast(mt.mode, mt.cnt, lo, mt.last)) {
+            nx.fast = true;
+            nx.a1 = __double_as_longlong(__ldg(&L.iv[r.g0 + lo + 1].E0));
+            nx.a2 = __double_as_longlong(__ldg(&L.iv[r.g0 + lo + 2].E0));
+        }
     }
 }
 
@@ -639,24 +664,31 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                 const int nst = (ncomp + LK_G - 1) / LK_G;
                 LkNext nx;
                 nx.valid = false;
-                if (lane < LK_G) lk_prefetch(L, e0, lane, ncomp, bmin, bmax, nx);
+                nx.fast = false;
+                if (lane < LK_G) lk_prefetch<true>(L, e0, lane, ncomp, bmin, bmax, nx);
                 for (int t = 0; t < nst; ++t, ++T) {
                     const int d = (int)(T % LK_D);
                     const LkNext cur = nx;
-                    if (lane < LK_G && t + 1 < nst) lk_prefetch(L, e0, (t + 1) * LK_G + lane, ncomp, bmin, bmax, nx);
+                    if (lane < LK_G && t + 1 < nst)
+                        lk_prefetch<true>(L, e0, (t + 1) * LK_G + lane, ncomp, bmin, bmax, nx);
                     if (T >= (uint32_t)LK_D) mbar_wait(&sh.empty[d], ((T / LK_D) - 1) & 1, 0x10000u | T);
                     uint32_t bytes = 0;
                     const bool copy_iv = lane < LK_G && cur.valid && cur.mt.mode != LK_GLOBAL;
+                    const bool fast = lane < LK_G && cur.valid && cur.fast;
+                    const uint32_t ncopy = fast ? 4u : (uint32_t)cur.mt.cnt;
                     if (lane < LK_G && cur.valid) {
                         sh.meta[d][lane] = cur.mt;
                         sh.word[d][lane] = lk_word(cur.mt.cnt, cur.mt.mode, cur.mt.lo, cur.mt.last);
+                        if (fast) sh.hdr[d][lane] = make_longlong2(cur.a1, cur.a2);
                     }
-                    if (copy_iv) bytes += (uint32_t)cur.mt.cnt * (uint32_t)sizeof(IvRec);
+                    const unsigned fb = __ballot_sync(0xffffffffu, fast);
+                    if (lane == 0) sh.sfast[d] = (fb & ((1u << LK_G) - 1u)) == ((1u << LK_G) - 1u);
+                    if (copy_iv) bytes += ncopy * (uint32_t)sizeof(IvRec);
                     if (DEN_ST && lane == 0) bytes += (uint32_t)lk_den_block(nmat);
                     mbar_arrive_tx(&sh.full[d], bytes);
                     if (copy_iv)
-                        bulk_g2s(&sh.iv[d][lane][0], L.iv + cur.mt.g0 + cur.mt.lo,
-                                 (uint32_t)cur.mt.cnt * (uint32_t)sizeof(IvRec), &sh.full[d]);
+                        bulk_g2s(&sh.iv[d][lane][0], L.iv + cur.mt.g0 + cur.mt.lo, ncopy * (uint32_t)sizeof(IvRec),
+                                 &sh.full[d]);
                     if (DEN_ST && lane == 0)
                         bulk_g2s(sden + (size_t)d * nmat * LK_DS, L.denS + (size_t)t * nmat * LK_DS,
                                  (uint32_t)lk_den_block(nmat), &sh.full[d]);
@@ -723,10 +755,37 @@ __global__ void __launch_bounds__(NW * 32, MINB)
             const int32_t bu = mine ? bin : bs;
             const int32_t mu = mine ? m : ms;
             double st = 0.0, sc = 0.0, sf = 0.0, snf = 0.0;
+            const long long Eb = __double_as_longlong(Eu);
             for (int t = 0; t < nst; ++t, ++T) {
                 const int d = (int)(T % LK_D);
                 mbar_wait(&sh.full[d], (T / LK_D) & 1, 0x20000u | T);
-                if (any) {
+                if (any && sh.sfast[d]) {
+                    // every nuclide of the stage is fast (lk_fast): no per-nuclide
+                    // meta word, clamp or branch -- the 8 folds' loads schedule freely
+#pragma unroll
+                    for (int j = 0; j < LK_G; ++j) {
+                        const int k = t * LK_G + j;
+                        const longlong2 ab = sh.hdr[d][j];
+                        const int32_t li = (int32_t)(ab.x <= Eb) + (int32_t)(ab.y <= Eb);
+                        const IvRec* a = sh.iv[d][j] + li;
+                        const double2 er = *reinterpret_cast<const double2*>(&a->E0);   // (E0, r)
+                        const double e1 = a[1].E0;
+                        const double2 tdt = *reinterpret_cast<const double2*>(&a->t0);
+                        const double2 cdc = *reinterpret_cast<const double2*>(&a->c0);
+                        const double2 fdf = *reinterpret_cast<const double2*>(&a->f0);
+                        const double fr = div_by_rcp_safe(__dsub_rn(Eu, er.x), __dsub_rn(e1, er.x), er.y);
+                        const double tt = __dadd_rn(tdt.x, __dmul_rn(fr, tdt.y));
+                        const double cc = __dadd_rn(cdc.x, __dmul_rn(fr, cdc.y));
+                        const double ff = __dadd_rn(fdf.x, __dmul_rn(fr, fdf.y));
+                        const double2 dd =
+                            DEN_ST ? *reinterpret_cast<const double2*>(sden + ((size_t)d * nmat + mu) * LK_DS + 2 * j)
+                                   : *reinterpret_cast<const double2*>(&L.ddT[(int64_t)k * nmat + mu]);
+                        st = __dadd_rn(st, __dmul_rn(dd.x, tt));
+                        sc = __dadd_rn(sc, __dmul_rn(dd.x, cc));
+                        sf = __dadd_rn(sf, __dmul_rn(dd.x, ff));
+                        snf = __dadd_rn(snf, __dmul_rn(dd.y, ff));
+                    }
+                } else if (any) {
 #pragma unroll
                     for (int j = 0; j < LK_G; ++j) {
                         const int k = t * LK_G + j;
@@ -754,6 +813,8 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                         sf = __dadd_rn(sf, __dmul_rn(dd.x, ff));
                         snf = __dadd_rn(snf, __dmul_rn(dd.y, ff));
                     }
+                }
+                if (any) {
                     constexpr int CKS = kCkptStride / LK_G;
                     if (ckon && (t + 1) % CKS == 0 && (t + 1) * LK_G <= ncomp) {
                         const int32_t row = (t + 1) / CKS - 1;
