@@ -540,7 +540,7 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
     c->lk_piped = true;
     if (const char* lp = getenv("EMC_LK_PIPED")) c->lk_piped = atoi(lp) != 0;
     c->lk_pcfg = 1;
-    if (const char* lp = getenv("EMC_LK_PCFG")) c->lk_pcfg = std::max(0, std::min(2, atoi(lp)));
+    if (const char* lp = getenv("EMC_LK_PCFG")) c->lk_pcfg = std::max(0, std::min(LK_NPCFG - 1, atoi(lp)));
     const char* ro = getenv("EMC_REORDER");
     c->reorder = !(ro && ro[0] == '0');
     if (c->reorder) rc |= c->ps2.alloc(nslots);

@@ -846,8 +846,10 @@ __global__ void __launch_bounds__(NW * 32, MINB)
 
 // piped configurations: 0 = one 32-warp CTA per SM, 1 = two 16-warp CTAs per SM
 // (their chunk boundaries overlap; needs the ring to fit twice in shared memory)
-constexpr int lk_pcfg_warps(int c) { return c == 1 ? 16 : c == 2 ? 10 : 32; }
-constexpr int lk_pcfg_minb(int c) { return c == 1 ? 2 : c == 2 ? 3 : 1; }
+// 3 = 16 x 1 (128 registers), 4 = 24 x 1 (80), 5 = 12 x 2 (80)
+constexpr int LK_NPCFG = 6;
+constexpr int lk_pcfg_warps(int c) { return c == 1 || c == 3 ? 16 : c == 2 ? 10 : c == 4 ? 24 : c == 5 ? 12 : 32; }
+constexpr int lk_pcfg_minb(int c) { return c == 1 || c == 5 ? 2 : c == 2 ? 3 : 1; }
 
 template <int MODE, int PC>
 inline cudaError_t lk_launch_piped_cfg(const DLib& L, const int32_t* q, int64_t n, DSlots S, int32_t fused,
@@ -872,10 +874,12 @@ inline cudaError_t lk_launch_piped(const DLib& L, const int32_t* q, int64_t n, D
                                    int sm_count, size_t smem, cudaStream_t st, PState* rdst, const LkKeys& K,
                                    int pcfg = 0)
 {
-    if (pcfg == 1)
-        return lk_launch_piped_cfg<MODE, 1>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, rdst, K);
-    if (pcfg == 2)
-        return lk_launch_piped_cfg<MODE, 2>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, rdst, K);
+    switch (pcfg) {
+#define EMC_PC(C) case C: return lk_launch_piped_cfg<MODE, C>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, rdst, K);
+    EMC_PC(1) EMC_PC(2) EMC_PC(3) EMC_PC(4) EMC_PC(5)
+#undef EMC_PC
+    default: break;
+    }
     return lk_launch_piped_cfg<MODE, 0>(L, q, n, S, fused, cnt, bE, bM, bout, sm_count, smem, st, rdst, K);
 }
 
@@ -943,19 +947,12 @@ inline cudaError_t lk_set_smem(size_t smem)
         (e = lk_set_smem_cfg<1, 2>(smem)) || (e = lk_set_smem_cfg<1, 3>(smem)))
         return e;
     const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
-    if ((e = cudaFuncSetAttribute(k_lookup_piped<0, true, 32, 1>, a, (int)smem)) ||
-        (e = cudaFuncSetAttribute(k_lookup_piped<0, false, 32, 1>, a, (int)smem)) ||
-        (e = cudaFuncSetAttribute(k_lookup_piped<1, true, 32, 1>, a, (int)smem)) ||
-        (e = cudaFuncSetAttribute(k_lookup_piped<1, false, 32, 1>, a, (int)smem)) ||
-        (e = cudaFuncSetAttribute(k_lookup_piped<0, true, 16, 2>, a, (int)smem)) ||
-        (e = cudaFuncSetAttribute(k_lookup_piped<0, false, 16, 2>, a, (int)smem)) ||
-        (e = cudaFuncSetAttribute(k_lookup_piped<1, true, 16, 2>, a, (int)smem)) ||
-        (e = cudaFuncSetAttribute(k_lookup_piped<1, false, 16, 2>, a, (int)smem)) ||
-        (e = cudaFuncSetAttribute(k_lookup_piped<0, true, 10, 3>, a, (int)smem)) ||
-        (e = cudaFuncSetAttribute(k_lookup_piped<0, false, 10, 3>, a, (int)smem)) ||
-        (e = cudaFuncSetAttribute(k_lookup_piped<1, true, 10, 3>, a, (int)smem)) ||
-        (e = cudaFuncSetAttribute(k_lookup_piped<1, false, 10, 3>, a, (int)smem)))
+#define EMC_PS(M, C) (e = cudaFuncSetAttribute(k_lookup_piped<M, true, lk_pcfg_warps(C), lk_pcfg_minb(C)>, a, (int)smem)) || \
+                     (e = cudaFuncSetAttribute(k_lookup_piped<M, false, lk_pcfg_warps(C), lk_pcfg_minb(C)>, a, (int)smem))
+    if (EMC_PS(0, 0) || EMC_PS(0, 1) || EMC_PS(0, 2) || EMC_PS(0, 3) || EMC_PS(0, 4) || EMC_PS(0, 5) ||
+        EMC_PS(1, 0) || EMC_PS(1, 1) || EMC_PS(1, 2) || EMC_PS(1, 3) || EMC_PS(1, 4) || EMC_PS(1, 5))
         return e;
+#undef EMC_PS
     return cudaSuccess;
 }
 
