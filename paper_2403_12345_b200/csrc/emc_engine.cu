@@ -186,6 +186,10 @@ struct emc_ctx {
     int64_t tail_warp_n = 32768; // tail queues up to this length use the warp-per-particle lookup (EMC_TAIL_WARP_N)
     int64_t tail_sub_n = 131072; // ... up to this length 8 lanes per particle (EMC_TAIL_SUB_N)
     bool all_small = false;      // no composition group is staged (all < LK_MIN_NUC): the gather kernel serves
+    // small-population finish (EMC_FINISH_N): a tail queue at most this long is
+    // carried to death by k_finish (one thread per particle) in one launch;
+    // -1 = by library (whole tail for gather-lookup libraries, off for staged ones)
+    int64_t finish_n = -1;
     cudaEvent_t evt[4 * 32]{};
     bool ev_init = false;
 };
@@ -217,6 +221,7 @@ extern "C" int emc_create(int device, emc_ctx** out)
     if (const char* t = getenv("EMC_TAIL_LOOKUP")) c->tail_plain = std::strcmp(t, "plain") == 0;
     if (const char* t = getenv("EMC_TAIL_WARP_N")) c->tail_warp_n = std::max<int64_t>(0, atoll(t));
     if (const char* t = getenv("EMC_TAIL_SUB_N")) c->tail_sub_n = std::max<int64_t>(0, atoll(t));
+    if (const char* t = getenv("EMC_FINISH_N")) c->finish_n = std::max<int64_t>(0, atoll(t));
     c->ev_init = true;
     *out = c;
     return 0;
@@ -787,6 +792,24 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
         int64_t look_inv = 0, tail_blocks = 0;
         float ms;
         while (nL > 0 && c->ctl_host->err == 0) {
+            const int64_t fin_n = c->finish_n >= 0 ? c->finish_n : (c->all_small ? c->tail_n : 0);
+            if (nL <= fin_n && c->ctl_host->cursor >= (unsigned long long)cf.n_assigned) {
+                // small population: finish every remaining history in one launch
+                EMC_TRY_CUDA(cudaEventRecord(c->ev[0], st));
+                k_finish<<<(unsigned)((nL + 127) / 128), 128, 0, st>>>(cur, nL, bp, c->L, c->G, c->S, lg, sv,
+                                                                       c->bins.p, c->ctl.p, c->cnt.p, c->M);
+                EMC_CHECK_LAUNCH(c);
+                EMC_TRY_CUDA(cudaEventRecord(c->ev[1], st));
+                EMC_TRY_CUDA(cudaMemsetAsync(&c->ctl.p->nL2, 0, sizeof(unsigned), st));
+                EMC_TRY_CUDA(cudaMemcpyAsync(c->ctl_host, c->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+                EMC_TRY_CUDA(cudaStreamSynchronize(st));
+                cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]);
+                tm[0] += ms * 1e-3;
+                host_cnt[CNT_INV_LOOKUP] += 1; host_cnt[CNT_INV_ADVANCE] += 1; host_cnt[CNT_INV_COLLISION] += 1;
+                iterations += 1;
+                nL = 0;
+                break;
+            }
             if (nL <= c->tail_n && c->ctl_host->cursor >= (unsigned long long)cf.n_assigned) {
                 // tail mode: tail_k iterations back to back, queue lengths on the device
                 const int K = c->tail_k;
