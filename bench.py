@@ -47,7 +47,9 @@ METRIC = "particles/s (active batches), HM-large depleted fuel, at 1/2/4/8 B200"
 GUARD_NOTE = ("box_guard on (RunConfig extension, include/emc.h): the reference's nudge can lose a particle "
               "outside the reflective box (~1 per 1e9 histories; seed 42 stops batch 22 without it, "
               "profiles/r2_c4_escape_replay.md); histories that stay inside are bit-identical to the reference")
-WORKLOAD = dict(workload="C4 HM-large depleted pincell: depleted_pincell(272,3,11303,100,seed=1)",
+WORKLOAD = dict(workload="C4 HM-large depleted fuel on the Hoogenboom-Martin core: hm_core(272,3,11303,100,seed=1): "
+                         "241 assemblies x 264 pins (17x17, 25 tubes), 323x323 pin lattice with water reflector, "
+                         "366 cm, 100 axial depleted-fuel zones, reflective",
                 ppb_per_gpu=40_000_000, mode="event", reduction="fast", tally_mode="fused",
                 sort="on (group, log E, mat) every lookup sweep", seed=42, box_guard=GUARD_NOTE)
 # --workload c5: BASELINE configs[4] (SURVEY 8f row 1 extension)
@@ -62,12 +64,11 @@ WORKLOAD_C5 = dict(workload="C5 shielding_slab(8 nuclides/material, 2000 points,
 METRIC_C1 = "particles/s (active batches), UO2 pincell, 12 fuel nuclides (C1)"
 WORKLOAD_C1 = dict(workload="C1 pincell: depleted_pincell(12,3,100,8,seed=1), 10k particles/batch", ppb_per_gpu=10_000,
                    mode="event", reduction="deterministic", seed=42, box_guard=GUARD_NOTE)
-# --workload c3: BASELINE configs[2] (Hoogenboom-Martin small restated on the pincell, SURVEY 8 "C3")
-METRIC_C3 = "particles/s (active batches), HM-small fresh fuel (34 fuel nuclides)"
-WORKLOAD_C3 = dict(workload="C3 HM-small pincell: depleted_pincell(34,3,11303,100,seed=1), 10M particles/batch "
-                            "(seed 42 stops in batch 5 without the box guard, profiles/r1s5_c3_reference_error.txt)",
-                   ppb_per_gpu=10_000_000,
-                   mode="event", reduction="fast", seed=42, box_guard=GUARD_NOTE)
+# --workload c3: BASELINE configs[2] (Hoogenboom-Martin small: fresh fuel, 34 fuel nuclides, HM core)
+METRIC_C3 = "particles/s (active batches), HM-small fresh fuel (34 fuel nuclides), HM core"
+WORKLOAD_C3 = dict(workload="C3 HM-small on the Hoogenboom-Martin core: hm_core(34,3,11303,100,seed=1), "
+                            "10M particles/batch",
+                   ppb_per_gpu=10_000_000, mode="event", reduction="fast", seed=42, box_guard=GUARD_NOTE)
 # --workload c2: BASELINE configs[1] (17x17 assembly, SURVEY 8f row 2 extension)
 METRIC_C2 = "particles/s (active batches), 2D 17x17 PWR assembly, ~30 nuclides"
 WORKLOAD_C2 = dict(workload="C2 pwr_assembly(27 fuel + 3 moderator nuclides, 11303 points, 17x17 lattice, "
@@ -75,17 +76,39 @@ WORKLOAD_C2 = dict(workload="C2 pwr_assembly(27 fuel + 3 moderator nuclides, 113
                    ppb_per_gpu=1_000_000, mode="event", reduction="fast", seed=42, box_guard=GUARD_NOTE)
 
 
+# --workload c4pin / c3pin: the same libraries on the reference's own geometry,
+# the single pin cell (kernels.py:418-492) with 100 axial zones in 10 cm
+METRIC_C4PIN = "particles/s (active batches), HM-large depleted fuel library on the reference pin cell"
+WORKLOAD_C4PIN = dict(workload="C4 library on the pincell: depleted_pincell(272,3,11303,100,seed=1)",
+                      ppb_per_gpu=40_000_000, mode="event", reduction="fast", tally_mode="fused",
+                      sort="on (group, log E, mat) every lookup sweep", seed=42, box_guard=GUARD_NOTE)
+METRIC_C3PIN = "particles/s (active batches), HM-small fresh fuel library (34 fuel nuclides) on the reference pin cell"
+WORKLOAD_C3PIN = dict(workload="C3 library on the pincell: depleted_pincell(34,3,11303,100,seed=1), 10M particles/batch "
+                               "(seed 42 stops in batch 5 without the box guard, profiles/r1s5_c3_reference_error.txt)",
+                      ppb_per_gpu=10_000_000, mode="event", reduction="fast", seed=42, box_guard=GUARD_NOTE)
+METRICS = {"c1": METRIC_C1, "c2": METRIC_C2, "c3": METRIC_C3, "c5": METRIC_C5, "c4pin": METRIC_C4PIN,
+           "c3pin": METRIC_C3PIN}
+WORKLOADS = {"c1": WORKLOAD_C1, "c2": WORKLOAD_C2, "c3": WORKLOAD_C3, "c5": WORKLOAD_C5, "c4pin": WORKLOAD_C4PIN,
+             "c3pin": WORKLOAD_C3PIN}
+
+
 def problem(args):
     import paper_2403_12345_b200 as P
+    if args.workload == "c4pin":
+        return P.depleted_pincell(272, 3, 11303, 100, seed=1)
+    if args.workload == "c3pin":
+        return P.depleted_pincell(34, 3, 11303, 100, seed=1)
     if args.workload == "c5":
         return P.shielding_slab()
     if args.workload == "c2":
         return P.pwr_assembly()
     if args.workload == "c3":
-        return P.depleted_pincell(34, 3, 11303, 100, seed=1)
+        return P.hm_core(34, 3, 11303, 100, seed=1)
     if args.workload == "c1":
         return P.depleted_pincell(12, 3, 100, 8, seed=1)
-    return P.depleted_pincell(272, 3, 11303, 100, seed=1)
+    return P.hm_core(272, 3, 11303, 100, seed=1)
+
+
 BYTES_PER_NUCLIDE_LOOKUP = 64
 # ncu counters of the XS-lookup kernels over one C4 batch of the CURRENT build
 # (tools/lookup_counters.py writes it with the hash of csrc/ it was captured on)
@@ -312,13 +335,13 @@ def run_reference(args):
     best = max(runs, key=lambda m: runs[m]["active_rate"])
     res = runs[best]
     v = res["active_rate"]
-    line = {"impl": "reference", "metric": {"c1": METRIC_C1, "c2": METRIC_C2, "c3": METRIC_C3, "c5": METRIC_C5}.get(args.workload, METRIC),
+    line = {"impl": "reference", "metric": METRICS.get(args.workload, METRIC),
             "value": v, "unit": "particles/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * res["active_wall"] / max(args.steps, 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": dict({"c1": WORKLOAD_C1, "c2": WORKLOAD_C2, "c3": WORKLOAD_C3, "c5": WORKLOAD_C5}.get(args.workload, WORKLOAD),
+            "config": dict(WORKLOADS.get(args.workload, WORKLOAD),
                            mode=best, reduction="deterministic (reference default)",
                            ppb_sample=ppb,
                            impl="C restatement of the reference kernels (oracle/, bit-exact with the "
@@ -344,7 +367,7 @@ def run_ours(args):
     lib, cell = problem(args)
     t_lib = time.perf_counter() - t0
     c5 = args.workload == "c5"
-    wl = {"c1": WORKLOAD_C1, "c2": WORKLOAD_C2, "c3": WORKLOAD_C3, "c5": WORKLOAD_C5}.get(args.workload, WORKLOAD)
+    wl = WORKLOADS.get(args.workload, WORKLOAD)
     ppb_gpu = args.particles or wl["ppb_per_gpu"]
     ext = dict(run_mode="fixed_source", mesh=WORKLOAD_C5["mesh"]) if c5 else dict(box_guard=True)
     cfg = P.RunConfig(particles_per_batch=ppb_gpu * ws, inactive_batches=args.warmup,
@@ -394,7 +417,7 @@ def run_ours(args):
     achieved = (BYTES_PER_NUCLIDE_LOOKUP * n_nl / ws) / lk_time / 1e9 if lk_time else None
     binding = lookup_counters(n_nl / ws, res.timings.get("lookup_launches_active", 0) / ws)
     line = {
-        "metric": {"c1": METRIC_C1, "c2": METRIC_C2, "c3": METRIC_C3, "c5": METRIC_C5}.get(args.workload, METRIC), "value": value,
+        "metric": METRICS.get(args.workload, METRIC), "value": value,
         "unit": "particles/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -428,7 +451,7 @@ def run_ours(args):
     if ws == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         line["cpu_baseline"] = cpu_baseline(args, lib, cell, threads, args.cpu_particles or (
-            10000 if args.workload in ("c4", "c3") else 4000) * threads)
+            10000 if args.workload in ("c4", "c3", "c4pin", "c3pin") else 4000) * threads)
     if c5:
         line["mesh"] = {"cells": int(np.prod(WORKLOAD_C5["mesh"])),
                         "flux_first_layer": float(res.mesh_mean[0, ..., 0].sum()),
@@ -444,7 +467,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--particles", type=int, default=0,
                     help="particles per GPU per batch (default 40M for c4, 10M for c5)")
-    ap.add_argument("--workload", default="c4", choices=("c4", "c1", "c2", "c3", "c5"),
+    ap.add_argument("--workload", default="c4", choices=("c4", "c1", "c2", "c3", "c5", "c4pin", "c3pin"),
                     help="c4: headline HM-large eigenvalue (BASELINE metric); c2: 17x17 assembly; "
                          "c3: HM-small; c5: fixed-source slab + mesh")
     ap.add_argument("--max-in-flight", type=int, default=0)

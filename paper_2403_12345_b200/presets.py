@@ -125,3 +125,56 @@ def pwr_assembly(n_fuel_nuclides: int = 27, n_moderator_nuclides: int = 3, gridp
                    fuel_material_ids=list(pin.fuel_material_ids),
                    moderator_material_id=pin.moderator_material_id, lattice=17, pin_map=pin_map)
     return library, cell
+
+
+# Hoogenboom-Martin core map: 241 fuel assemblies in a 17 x 17 assembly grid
+# (row lengths, centred; the 48 corner positions are water)
+HM_CORE_ROWS = (7, 11, 13, 15, 15, 17, 17, 17, 17, 17, 17, 17, 15, 15, 13, 11, 7)
+
+
+def hm_assembly_map(core_rows=HM_CORE_ROWS, reflector: int = 1) -> list[list[int]]:
+    """Assembly grid of the core plus `reflector` rings of water assemblies:
+    1 = fuel assembly, 0 = water."""
+    n = len(core_rows)
+    m = n + 2 * reflector
+    grid = [[0] * m for _ in range(m)]
+    for r, k in enumerate(core_rows):
+        lo = (n - k) // 2
+        for c in range(lo, lo + k):
+            grid[reflector + r][reflector + c] = 1
+    return grid
+
+
+def hm_core(n_fuel_nuclides: int = 272, n_moderator_nuclides: int = 3, gridpoints: int = 11303,
+            n_axial: int = 100, seed: int = 1, core_rows=HM_CORE_ROWS, reflector: int = 1,
+            height: float = 366.0) -> tuple[Library, Pincell]:
+    """Hoogenboom-Martin-style full core (BASELINE configs 3 and 4; SURVEY 8f
+    row 2): 241 17x17 fuel assemblies (264 fuel pins + 25 guide/instrument
+    tubes each, pitch 1.26 cm) in a 17 x 17 assembly grid with water corners,
+    one ring of water-reflector assemblies, 366 cm tall with `n_axial` axial
+    fuel zones (one depleted-fuel material each, the depleted_pincell
+    generator and seeds), reflective outer planes.  The assembly pitch is
+    exactly 17 pin pitches, so the two-level lattice (core -> assembly -> pin)
+    is one global pin lattice of (17 + 2 * reflector) * 17 cells per side whose
+    pin map is the assembly map expanded by the assembly's own pin map: the
+    device's lattice tracking (one integer cell index per axis) serves it
+    unchanged."""
+    library, pin = depleted_pincell(n_fuel_nuclides, n_moderator_nuclides, gridpoints, n_axial, seed)
+    amap = hm_assembly_map(core_rows, reflector)
+    na = len(amap)
+    n = na * 17
+    apin = [1] * (17 * 17)
+    for r, c in PWR_17_WATER_HOLES:
+        apin[r * 17 + c] = 0
+    pin_map = [0] * (n * n)
+    for ar in range(na):
+        for ac in range(na):
+            if not amap[ar][ac]:
+                continue
+            for r in range(17):
+                row = (ar * 17 + r) * n + ac * 17
+                pin_map[row:row + 17] = apin[r * 17:(r + 1) * 17]
+    cell = Pincell(fuel_radius=pin.fuel_radius, pitch=pin.pitch, height=height, n_axial=n_axial,
+                   fuel_material_ids=list(pin.fuel_material_ids),
+                   moderator_material_id=pin.moderator_material_id, lattice=n, pin_map=pin_map)
+    return library, cell
