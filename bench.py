@@ -1,17 +1,20 @@
 """Benchmark: active-batch particles/s on HM-large depleted fuel (C4).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload W]
     torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU, NCCL)
 
 Workload (BASELINE.json configs[3], SURVEY.md section 8 "C4"): library
-depleted_pincell(272 fuel, 3 moderator, 11303 grid points, 100 axial) seed 1,
+depleted_pincell generator (272 fuel, 3 moderator nuclides, 11303 grid
+points, 100 axial depleted-fuel materials) seed 1 on the Hoogenboom-Martin
+core (presets.hm_core: 241 17x17 assemblies, 323x323 pin lattice, 366 cm),
 k-eigenvalue, event mode, sorted lookups, fused tallies, fast (atomic)
 reduction, 40M particles per GPU per batch (weak scaling: ppb = N x 40M).
+--workload c4pin runs the same library on the reference's own pin cell.
 A step is one active batch; W warm-up batches (inactive: batch 0 samples the
 source from scratch, later ones resample the bank) precede K timed active
 batches.  The library (99.5 MB of grid records) is resident in HBM and every
-batch re-reads it >100x over through ~40M x 10.5 lookups, so inputs are far
-larger than L2 in aggregate traffic; no flush between batches is needed.
+batch re-reads it >100x over, so inputs are far larger than L2 in aggregate
+traffic; no flush between batches is needed.
 
 value     = K*ppb / device time of the K active batches (CUDA events on the
             engine stream, max over ranks)
@@ -19,12 +22,14 @@ e2e       = RunResult.active_rate of the same run_event() call: the
             reference's own metric definition (replication.py:282-304, host
             wall per batch incl. host merge/reduce/resample and the per-batch
             D2H of counters/tallies), i.e. through the public API.
-roofline  = XS-lookup kernel (k_lookup_piped; k_lookup_staged on unsorted tail queues): algorithmic bytes = 64 B per
-            (lookup, nuclide) (grid pair + sigma_t/c/f pairs) / summed
-            lookup time.  The staged kernel re-reads each record from shared
-            memory for ~1000 particles, so achieved > HBM peak: the kernel is
-            bound by the shared-memory (L1TEX) data pipe and FP64 issue, not by
-            DRAM (see DESIGN.md section 4 and profiles/).
+roofline  = the XS lookup (k_lookup_piped; tail kernels on unsorted queues),
+            bound by the L1TEX data pipe that serves the shared-memory-staged
+            interval records: ncu wavefronts per nuclide-lookup (sampled on
+            this build right after the timed region, tools/lookup_counters.py)
+            x the run's nuclide-lookups x 128 B / the run's summed lookup time,
+            against the pipe's peak.  `hbm` keeps north_star's gather model
+            (64 B per nuclide-lookup: > HBM peak because staged
+            records serve ~1000 particles per DRAM read) and measured DRAM.
 """
 
 from __future__ import annotations
@@ -32,6 +37,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import shutil
 import statistics
 import subprocess
 import sys
@@ -126,27 +132,37 @@ def csrc_hash() -> str:
     return h.hexdigest()[:16]
 
 
-def lookup_counters(nl_per_step: float, launches_per_step: float) -> dict:
-    """The XS lookup's binding unit from ncu (profiles/LOOKUP_COUNTERS): DRAM
-    bytes and shared-memory wavefronts per nuclide-lookup, L1TEX throughput.
-    Counters cannot be read inside a timed run; the file records the source
-    hash it was captured on and `current` says whether that is this build."""
+def lookup_counters(args, ppb: int) -> dict:
+    """ncu counters of the XS lookup of THIS build, per nuclide-lookup
+    (tools/lookup_counters.py): measured right after the timed region on a
+    sample of full-population k_lookup_piped launches of one batch of the same
+    workload in a child process (counters cannot be read inside a timed run);
+    if ncu is unavailable, the committed profiles/LOOKUP_COUNTERS capture,
+    flagged `current` when it was taken on this source hash."""
+    err = None
+    if not args.no_counters and shutil.which("ncu") and not os.environ.get("CUDA_INJECTION64_PATH"):
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        try:
+            import lookup_counters as LC
+            import tempfile
+            with tempfile.TemporaryDirectory() as td:
+                prof = LC.capture(ppb, args.workload, sample=(2, 4), timeout=240, log=os.path.join(td, "lc.csv"))
+            prof["source"] = "live: " + prof["command"]
+            prof["current"] = True
+            return prof
+        except Exception as e:  # noqa: BLE001
+            err = f"{type(e).__name__}: {str(e)[:200]}"
     path = os.path.join(ROOT, "profiles", LOOKUP_COUNTERS)
     try:
         with open(path) as fh:
             prof = json.load(fh)
     except (OSError, ValueError):
-        return {"source": None}
-    out = {k: prof.get(k) for k in ("l1tex_throughput_pct", "dram_bytes_per_nuclide_lookup",
-                                     "shared_wavefronts_per_warp_nuclide", "design_min_wavefronts_per_warp_nuclide",
-                                     "fp64_pipe_pct", "issue_active_pct")}
-    out["unit"] = "L1TEX / shared-memory data pipe"
-    out["source"] = f"profiles/{LOOKUP_COUNTERS} ({prof.get('command', 'ncu')})"
-    out["current"] = prof.get("csrc_hash") == csrc_hash()
-    b = prof.get("dram_bytes_per_nuclide_lookup")
-    if b is not None and launches_per_step:
-        out["dram_bytes_per_launch"] = b * nl_per_step / launches_per_step
-    return out
+        return {"source": None, "error": err}
+    prof["source"] = f"profiles/{LOOKUP_COUNTERS} ({prof.get('command', 'ncu')})"
+    prof["current"] = prof.get("csrc_hash") == csrc_hash()
+    if err:
+        prof["live_error"] = err
+    return prof
 
 
 def _peaks():
@@ -415,7 +431,20 @@ def run_ours(args):
     peak, peak_src = _peaks()
     lk_time = res.timings["lookup_active_s"] / ws if "lookup_active_s" in res.timings else None
     achieved = (BYTES_PER_NUCLIDE_LOOKUP * n_nl / ws) / lk_time / 1e9 if lk_time else None
-    binding = lookup_counters(n_nl / ws, res.timings.get("lookup_launches_active", 0) / ws)
+    clocks = sampler.summary()
+    # roofline: the lookup's binding unit is the L1TEX data pipe (shared-memory
+    # staged records), not HBM -- wavefronts per nuclide-lookup from ncu on this
+    # build x this run's nuclide-lookups / this run's lookup time (CUDA events)
+    prof = lookup_counters(args, ppb_gpu) if ws == 1 and not c5 else {"source": None}
+    wf = prof.get("l1_wavefronts_per_nuclide_lookup")
+    l1_peak = l1_ach = None
+    if wf and prof.get("l1_wavefront_peak_per_cycle") and lk_time:
+        clk = (clocks.get("sm_mhz") or 0) * 1e6 or prof.get("sm_clock_hz")
+        l1_peak = prof["l1_wavefront_peak_per_cycle"] * 128 * clk / 1e9
+        l1_ach = wf * 128 * (n_nl / ws) / lk_time / 1e9
+    nlaunch = res.timings.get("lookup_launches_active", 0) / ws
+    dram_nl = prof.get("dram_bytes_per_nuclide_lookup")
+    dram_gbs = dram_nl * (n_nl / ws) / lk_time / 1e9 if dram_nl and lk_time else None
     line = {
         "metric": METRICS.get(args.workload, METRIC), "value": value,
         "unit": "particles/s", "n_gpus": ws,
@@ -430,20 +459,32 @@ def run_ours(args):
                 "d2h_bytes_per_step": res.timings.get("d2h_bytes_active", 0) / max(args.steps, 1),
                 "d2h_bytes_final_bank": res.timings.get("d2h_bytes_final_bank", 0)},
         "gpu_launches": int(launches0["end"] - launches0["n"]),
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None,
-                     "traffic": binding.pop("dram_bytes_per_launch", None),
+        "roofline": {"bound": "l1tex", "achieved": l1_ach, "peak": l1_peak, "unit": "GB/s",
+                     "frac": (l1_ach / l1_peak) if l1_ach and l1_peak else None,
+                     "traffic": dram_nl * (n_nl / ws) / nlaunch if dram_nl and nlaunch else None,
                      "kernel": "XS lookup: every lookup launch of the active batches (k_lookup_piped on sorted "
-                               "sweeps, k_lookup_staged / k_lookup_warp on unsorted tail queues), summed",
-                     "peak_source": peak_src,
-                     "algorithmic_bytes": "64 B x nuclide-lookups (grid pair + sigma_t,c,f pairs, SURVEY 8d)",
-                     "meaning": "north_star's HBM gather roofline: algorithmic gather bytes / lookup time vs HBM "
-                                "peak; frac > 1 because the staged kernel reads each record from DRAM once per "
-                                "chunk and serves ~1000 particles from shared memory. The binding unit is "
-                                "the L1TEX/shared-memory pipe (see 'binding')",
-                     "nuclide_lookups_per_step": n_nl / args.steps,
-                     "binding": binding},
-        "clocks": sampler.summary(),
+                               "sweeps, k_lookup_staged / k_lookup_warp on unsorted tail queues), time summed "
+                               "from CUDA events on the engine stream",
+                     "meaning": "L1TEX data-pipe bytes delivered (128 B per wavefront; ncu wavefronts per "
+                                "nuclide-lookup of this build x this run's nuclide-lookups) / lookup time, vs the "
+                                "data pipe's peak (wavefronts per cycle x 128 B x live SM clock): the staged "
+                                "lookup serves every interval record from shared memory, so this pipe -- not "
+                                "HBM -- binds it",
+                     "counters": {k: prof.get(k) for k in (
+                         "source", "current", "live_error", "l1_wavefronts_per_warp_nuclide",
+                         "shared_wavefronts_per_warp_nuclide", "design_min_wavefronts_per_warp_nuclide",
+                         "l1tex_data_pipe_pct", "fp64_pipe_pct", "issue_active_pct",
+                         "warp_instructions_per_warp_nuclide", "dram_bytes_per_nuclide_lookup") if k in prof},
+                     "hbm": {"peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                             "algorithmic": achieved,
+                             "algorithmic_frac": (achieved / peak) if achieved else None,
+                             "algorithmic_bytes": "64 B x nuclide-lookups (grid pair + sigma_t,c,f pairs, "
+                                                  "SURVEY 8d); > peak because each staged record byte read from "
+                                                  "DRAM serves ~1000 particles",
+                             "dram_measured": dram_gbs,
+                             "dram_frac": (dram_gbs / peak) if dram_gbs else None},
+                     "nuclide_lookups_per_step": n_nl / args.steps},
+        "clocks": clocks,
         "k_mean": res.k_mean, "k_stderr": res.k_stderr,
         "box_guard_events": res.counters.get("box_guard"),
         "timings_s": {k: v for k, v in res.timings.items() if isinstance(v, float)},
@@ -474,6 +515,8 @@ def main():
     ap.add_argument("--cpu-particles", type=int, default=0)
     ap.add_argument("--ref-particles", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-counters", action="store_true",
+                    help="skip the post-run ncu sample of the lookup (roofline counters)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

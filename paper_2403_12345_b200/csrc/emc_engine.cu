@@ -944,8 +944,12 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             EMC_TRY_CUDA(cudaStreamSynchronize(st));
             cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]); tm[3] += ms * 1e-3;
             cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]); tm[0] += ms * 1e-3;
-            if (c->trace) std::fprintf(stderr, "emc-trace iter %lld nL %lld lookup_ms %.4f\n", (long long)iterations,
-                                       (long long)nL, ms);
+            if (c->trace) {       // + the iteration's nuclide-lookups (lookup_counters.py matches ncu launches)
+                unsigned long long nlc = 0;
+                cudaMemcpy(&nlc, c->cnt.p + CNT_NUCLIDE_LOOKUPS, sizeof(nlc), cudaMemcpyDeviceToHost);
+                std::fprintf(stderr, "emc-trace iter %lld nL %lld lookup_ms %.4f sorted %d nl_cum %llu\n",
+                             (long long)iterations, (long long)nL, ms, (int)do_sort, nlc);
+            }
             cudaEventElapsedTime(&ms, c->ev[2], c->ev[3]); tm[1] += ms * 1e-3;
             cudaEventElapsedTime(&ms, c->ev[3], c->ev[4]); tm[2] += ms * 1e-3;
             int64_t nC = c->ctl_host->nC;

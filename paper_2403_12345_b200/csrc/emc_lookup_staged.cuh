@@ -762,11 +762,18 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                 if (any && sh.sfast[d]) {
                     // every nuclide of the stage is fast (lk_fast): no per-nuclide
                     // meta word, clamp or branch -- the 8 folds' loads schedule freely
+                    // brackets of all 8 nuclides first (independent broadcast loads,
+                    // 2 bits each), so no record load waits on its own header load
+                    uint32_t lis = 0;
+#pragma unroll
+                    for (int j = 0; j < LK_G; ++j) {
+                        const longlong2 ab = sh.hdr[d][j];
+                        lis |= ((uint32_t)(ab.x <= Eb) + (uint32_t)(ab.y <= Eb)) << (2 * j);
+                    }
 #pragma unroll
                     for (int j = 0; j < LK_G; ++j) {
                         const int k = t * LK_G + j;
-                        const longlong2 ab = sh.hdr[d][j];
-                        const int32_t li = (int32_t)(ab.x <= Eb) + (int32_t)(ab.y <= Eb);
+                        const int32_t li = (int32_t)((lis >> (2 * j)) & 3u);
                         const IvRec* a = sh.iv[d][j] + li;
                         const double2 er = *reinterpret_cast<const double2*>(&a->E0);   // (E0, r)
                         const double e1 = a[1].E0;
