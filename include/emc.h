@@ -171,6 +171,17 @@ int emc_bank_copy(emc_ctx *ctx, int64_t start, int64_t n, int64_t *parent, int32
                   double *E);
 
 /* --- single-operation entry points (public API wrappers) --- */
+/* Union-grid lookup backends (RunConfig.accel != "binary"; replication.py
+ * _union_for R:145-152 -> xslib.union_tuple X:166-172): the union energy grid
+ * ugrid[n] (strictly ascending), the bracket map map[n][n_nuclides]
+ * (build_unionized_index, X:321-339) and, for "unionized", the merged bounding
+ * channels merged[n][n_nuclides][8] (merge_channels X:342-358; nullable).
+ * Replaced by the next library upload. */
+int emc_upload_union(emc_ctx *ctx, const double *ugrid, int64_t n, const int32_t *map, const double *merged);
+/* lookup backend of transport and emc_xs_lookup: 0 binary (the device's
+ * log-hash + scan, bit-identical to the binary search), 1 double_index,
+ * 2 unionized (kernels.py ACCEL_* codes; K:306-320) */
+int emc_set_accel(emc_ctx *ctx, int32_t accel);
 /* kernels.macro_lookup_full (kernels.py:287-331): sums[n][5], partials[n][max_comp][4] (nullable) */
 int emc_xs_lookup(emc_ctx *ctx, int64_t n, const int32_t *mats, const double *E, double *sums,
                   double *partials, int32_t max_comp);

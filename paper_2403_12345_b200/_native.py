@@ -82,6 +82,8 @@ SYMBOLS = {
     "emc_bank_copy": (C.c_int, [_P, _I64, _I64] + [_P] * 9),
     "emc_xs_lookup": (C.c_int, [_P, _I64, _P, _P, _P, _P, _I32]),
     "emc_grid_index": (C.c_int, [_P, _I64, _P, _P, _P]),
+    "emc_upload_union": (C.c_int, [_P, _P, _I64, _P, _P]),
+    "emc_set_accel": (C.c_int, [_P, _I32]),
     "emc_locate": (C.c_int, [_P, _I64, _P, _P]),
     "emc_distance": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P]),
     "emc_particle_ops": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P]),

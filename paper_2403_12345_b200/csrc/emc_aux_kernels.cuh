@@ -131,7 +131,8 @@ __global__ void k_api_bracket(DLib L, int64_t n, const int32_t* __restrict__ ent
 }
 
 // K:287-331 macro_lookup_full: five sums + per-entry (t, s, c, f) partials
-__global__ void k_api_macro(DLib L, int64_t n, const int32_t* __restrict__ mats,
+template <int ACCEL>   // 0 log-hash (binary-search equivalent), 1 double_index, 2 unionized (X:292-318)
+__global__ void k_api_macro(DLib L, DUnion U, int64_t n, const int32_t* __restrict__ mats,
                             const double* __restrict__ E, int32_t max_comp, double* __restrict__ sums,
                             double* __restrict__ parts)
 {
@@ -141,17 +142,38 @@ __global__ void k_api_macro(DLib L, int64_t n, const int32_t* __restrict__ mats,
     double e = E[q];
     int32_t e0 = L.mat_off[m], e1 = L.mat_off[m + 1];
     int32_t bin = energy_bin(e, L);
+    const int64_t uj = ACCEL ? union_interval(U, L, e) : 0;
     double st = 0.0, ss = 0.0, sc = 0.0, sf = 0.0, snf = 0.0;
     for (int32_t k = e0; k < e1; ++k) {
         const Comp c = L.comp[k];
-        Rec r0, r1; int32_t gi;
-        int cl = bracket(L, c, bin, e, gi, r0, r1);
         double t, s, cc, f;
-        if (cl) { t = r0.t; s = L.ch_s[gi]; cc = r0.c; f = r0.f; }
-        else {
-            double fr = frac(e, r0.E, r1.E);
-            t = lerp(r0.t, r1.t, fr); s = lerp(L.ch_s[gi], L.ch_s[gi + 1], fr);
-            cc = lerp(r0.c, r1.c, fr); f = lerp(r0.f, r1.f, fr);
+        if (ACCEL == 0) {
+            Rec r0, r1; int32_t gi;
+            int cl = bracket(L, c, bin, e, gi, r0, r1);
+            if (cl) { t = r0.t; s = L.ch_s[gi]; cc = r0.c; f = r0.f; }
+            else {
+                double fr = frac(e, r0.E, r1.E);
+                t = lerp(r0.t, r1.t, fr); s = lerp(L.ch_s[gi], L.ch_s[gi + 1], fr);
+                cc = lerp(r0.c, r1.c, fr); f = lerp(r0.f, r1.f, fr);
+            }
+        } else {        // K:216-254: end clamps on the nuclide grid, then the mapped bracket
+            const Rec* R = L.rec + c.g0;
+            const int32_t last = c.glen - 1;
+            if (e <= R[0].E) { t = R[0].t; s = L.ch_s[c.g0]; cc = R[0].c; f = R[0].f; }
+            else if (e >= R[last].E) { t = R[last].t; s = L.ch_s[c.g0 + last]; cc = R[last].c; f = R[last].f; }
+            else {
+                const int32_t i = U.map[uj * U.n_nuc + c.nid];
+                const Rec r0 = R[i], r1 = R[i + 1];
+                const double fr = frac(e, r0.E, r1.E);
+                if (ACCEL == 2) {
+                    const double* mg = U.merged + (uj * U.n_nuc + c.nid) * 8;
+                    t = lerp(mg[0], mg[1], fr); s = lerp(mg[2], mg[3], fr);
+                    cc = lerp(mg[4], mg[5], fr); f = lerp(mg[6], mg[7], fr);
+                } else {
+                    t = lerp(r0.t, r1.t, fr); s = lerp(L.ch_s[c.g0 + i], L.ch_s[c.g0 + i + 1], fr);
+                    cc = lerp(r0.c, r1.c, fr); f = lerp(r0.f, r1.f, fr);
+                }
+            }
         }
         double pt = __dmul_rn(c.den, t);
         st = __dadd_rn(st, pt);

@@ -114,6 +114,10 @@ struct emc_ctx {
     DBuf<int32_t> mat_group, grp_off; DBuf<NucRef> gnuc; DBuf<DD> ddT; DBuf<double> denS; DBuf<IvRec> iv; DBuf<int32_t> nsafe;
     int32_t n_groups = 0;
     DLib L{};
+    // union-grid lookup backends (RunConfig.accel, emc_upload_union / emc_set_accel)
+    DUnion U{};
+    DBuf<double> u_grid, u_merged; DBuf<int32_t> u_hash, u_map;
+    int32_t n_nuc = 0;
     int32_t n_materials = 0, max_comp = 0, n_entries = 0;
     double nu_max = 0.0;         // largest nu of the library (bounds the fission-site ordinal)
     int64_t lib_bytes = 0;
@@ -423,6 +427,9 @@ extern "C" int emc_upload_library(emc_ctx* c, const emc_library* lib)
     for (int64_t i = 0; i < nn; ++i) c->nu_max = std::max(c->nu_max, lib->nu[i]);
     c->lib_bytes = (int64_t)(np * (sizeof(Rec) + 8) + hcomp.size() * sizeof(Comp) + hhash.size() * 4);
     c->have_lib = true;
+    c->n_nuc = (int32_t)nn;
+    c->u_grid.release(); c->u_merged.release(); c->u_hash.release(); c->u_map.release();
+    c->U = DUnion{};
     return 0;
 }
 
@@ -541,7 +548,8 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
     int rc = 0;
     rc |= c->ps.alloc(nslots);
     if (const char* lb = getenv("EMC_LOOKUP_BLOCK")) c->lookup_block = atoi(lb);
-    if (const char* lk = getenv("EMC_LOOKUP")) c->staged = std::strcmp(lk, "plain") != 0;
+    c->staged = c->U.accel == 0;      // the union backends use the one-thread-per-particle gather
+    if (const char* lk = getenv("EMC_LOOKUP")) c->staged = c->staged && std::strcmp(lk, "plain") != 0;
     c->lk_piped = true;
     if (const char* lp = getenv("EMC_LK_PIPED")) c->lk_piped = atoi(lp) != 0;
     c->lk_pcfg = 1;
@@ -818,7 +826,15 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
                     k_tail_begin<<<1, 1, 0, st>>>(c->ctl.p, c->cnt.p);
                     EMC_CHECK_LAUNCH(c);
                     EMC_TRY_CUDA(cudaEventRecord(c->evt[4 * k], st));
-                    if (nL <= c->tail_warp_n) {
+                    if (c->U.accel) {
+                        if (c->U.accel == 2)
+                            k_lookup_union<true><<<gl, 256, 0, st>>>(cur, (int32_t)nL, c->L, c->U, c->S, cf.fused,
+                                                                     c->cnt.p, &c->ctl.p->nLcur);
+                        else
+                            k_lookup_union<false><<<gl, 256, 0, st>>>(cur, (int32_t)nL, c->L, c->U, c->S, cf.fused,
+                                                                      c->cnt.p, &c->ctl.p->nLcur);
+                        EMC_TRY_CUDA(cudaGetLastError());
+                    } else if (nL <= c->tail_warp_n) {
                         // sparse tail: one warp per particle (latency of one fold, not of 272 gathers)
                         k_lookup_warp<32><<<grid_for(nL * 32, 256, 8 * c->sm_count), 256, 0, st>>>(
                             cur, (int32_t)nL, c->L, c->S, cf.fused, c->cnt.p, &c->ctl.p->nLcur);
@@ -910,6 +926,12 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
                     c->S.ps = rdst;
                     q = c->iota.p;
                 }
+            } else if (c->U.accel == 2) {
+                k_lookup_union<true><<<grid_for(nL, 256, maxb), 256, 0, st>>>(q, (int32_t)nL, c->L, c->U, c->S,
+                                                                             cf.fused, c->cnt.p, nullptr);
+            } else if (c->U.accel == 1) {
+                k_lookup_union<false><<<grid_for(nL, 256, maxb), 256, 0, st>>>(q, (int32_t)nL, c->L, c->U, c->S,
+                                                                              cf.fused, c->cnt.p, nullptr);
             } else switch (c->lookup_block) {
             case 1024:
                 k_lookup<1024><<<grid_for(nL, 1024, c->sm_count), 1024, 0, st>>>(q, (int32_t)nL, c->L, c->S,
@@ -1175,6 +1197,51 @@ int to_host(T* h, const DBuf<T>& b, int64_t n, cudaStream_t st)
 }
 }  // namespace
 
+extern "C" int emc_upload_union(emc_ctx* c, const double* ugrid, int64_t n, const int32_t* map,
+                                const double* merged)
+{
+    if (!c || !c->have_lib) return fail_arg("upload a library first");
+    if (!ugrid || !map || n < 1) return fail_arg("emc_upload_union: bad arguments");
+    const int64_t nn = c->n_nuc;
+    for (int64_t i = 1; i < n; ++i)
+        if (!(ugrid[i - 1] < ugrid[i])) return fail_arg("union grid must be strictly ascending");
+    if (n * nn > ((int64_t)1 << 40)) { g_err = "union index too large"; return EMC_E_RANGE; }
+    EMC_TRY_CUDA(cudaSetDevice(c->device));
+    // log-hash of the union grid with the library's integer bin map (exact
+    // lower bounds of searchsorted(right) - 1, as for the nuclide grids)
+    const int64_t nbins = c->L.nbins;
+    std::vector<int32_t> hh(nbins);
+    int64_t j = 0;
+    for (int64_t b = 0; b < nbins; ++b) {
+        uint64_t eb = (uint64_t)(c->L.key_lo + b) << c->L.shift;
+        double edge;
+        std::memcpy(&edge, &eb, 8);
+        while (j < n && ugrid[j] <= edge) ++j;
+        int64_t start = b == 0 ? 0 : std::max<int64_t>(0, j - 1);
+        hh[b] = (int32_t)std::min<int64_t>(start, std::max<int64_t>(0, n - 2));
+    }
+    c->u_grid.release(); c->u_merged.release(); c->u_hash.release(); c->u_map.release();
+    if (c->u_grid.alloc(n) || c->u_hash.alloc(nbins) || c->u_map.alloc(n * nn) ||
+        (merged && c->u_merged.alloc(n * nn * 8)))
+        return EMC_E_OOM;
+    EMC_TRY_CUDA(cudaMemcpy(c->u_grid.p, ugrid, n * sizeof(double), cudaMemcpyHostToDevice));
+    EMC_TRY_CUDA(cudaMemcpy(c->u_hash.p, hh.data(), nbins * sizeof(int32_t), cudaMemcpyHostToDevice));
+    EMC_TRY_CUDA(cudaMemcpy(c->u_map.p, map, n * nn * sizeof(int32_t), cudaMemcpyHostToDevice));
+    if (merged) EMC_TRY_CUDA(cudaMemcpy(c->u_merged.p, merged, n * nn * 8 * sizeof(double), cudaMemcpyHostToDevice));
+    c->U = DUnion{c->u_grid.p, c->u_hash.p, c->u_map.p, merged ? c->u_merged.p : nullptr, n, (int32_t)nn, 0};
+    return 0;
+}
+
+extern "C" int emc_set_accel(emc_ctx* c, int32_t accel)
+{
+    if (!c) return fail_arg("emc_set_accel: no context");
+    if (accel < 0 || accel > 2) return fail_arg("accel must be 0 (binary), 1 (double_index) or 2 (unionized)");
+    if (accel >= 1 && !c->U.ugrid) return fail_arg("accel needs a union index (emc_upload_union)");
+    if (accel == 2 && !c->U.merged) return fail_arg("accel = unionized needs merged channels");
+    c->U.accel = accel;
+    return 0;
+}
+
 extern "C" int emc_xs_lookup(emc_ctx* c, int64_t n, const int32_t* mats, const double* E, double* sums,
                              double* partials, int32_t max_comp)
 {
@@ -1190,8 +1257,15 @@ extern "C" int emc_xs_lookup(emc_ctx* c, int64_t n, const int32_t* mats, const d
     if (partials && dp.alloc(std::max<int64_t>(1, n * max_comp * 4))) return EMC_E_OOM;
     if (partials) EMC_TRY_CUDA(cudaMemsetAsync(dp.p, 0, n * max_comp * 4 * 8, st));
     if (n) {
-        k_api_macro<<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(c->L, n, dm.p, de.p, max_comp, ds.p,
-                                                                 partials ? dp.p : nullptr);
+        if (c->U.accel == 2)
+            k_api_macro<2><<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(c->L, c->U, n, dm.p, de.p, max_comp, ds.p,
+                                                                      partials ? dp.p : nullptr);
+        else if (c->U.accel == 1)
+            k_api_macro<1><<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(c->L, c->U, n, dm.p, de.p, max_comp, ds.p,
+                                                                      partials ? dp.p : nullptr);
+        else
+            k_api_macro<0><<<grid_for(n, 128, 1 << 30), 128, 0, st>>>(c->L, c->U, n, dm.p, de.p, max_comp, ds.p,
+                                                                      partials ? dp.p : nullptr);
         EMC_CHECK_LAUNCH(c);
     }
     to_host(sums, ds, n * 5, st);

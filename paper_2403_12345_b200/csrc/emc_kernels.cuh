@@ -257,6 +257,31 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_lookup(const int32_t* __restr
     warp_add_u64(cnt + CNT_NUCLIDE_LOOKUPS, nl);
 }
 
+// Lookup through the union grid (accel = double_index / unionized): one
+// thread per particle, like k_lookup.
+template <bool MERGED>
+__global__ void __launch_bounds__(256) k_lookup_union(const int32_t* __restrict__ q, int32_t n, DLib L, DUnion U,
+                                                      DSlots S, int32_t fused, unsigned long long* cnt,
+                                                      const unsigned int* nptr)
+{
+    if (nptr) n = (int32_t)*nptr;
+    unsigned long long nl = 0;
+    EMC_WARP_LOOP(n) {
+        int64_t i = emc_base_ + lane_id();
+        if (i < n) {
+            int32_t s = q[i];
+            double E = S.ps[s].a.E;
+            int32_t m = S.ps[s].d.mat;
+            P2 c;
+            macro_tcf_union<MERGED>(L, U, m, E, c.t, c.c, c.f, c.nsf, fused ? S.ckpt + s : nullptr, S.nck, S.nslots);
+            S.ps[s].c = c;
+            nl += (unsigned long long)(__ldg(L.mat_off + m + 1) - __ldg(L.mat_off + m));
+        }
+    }
+    warp_add_u64(cnt + CNT_INTERP_TRANSPORT, 4ull * nl);
+    warp_add_u64(cnt + CNT_NUCLIDE_LOOKUPS, nl);
+}
+
 // Warp-per-particle lookup for the sparse tail of a batch: a lone fuel
 // particle's 272-nuclide fold through the global path is ~272 dependent
 // gathers long, which sets the duration of every small tail iteration.  Here

@@ -45,6 +45,8 @@ class DeviceEngine:
         self._src_keep = None
         self.library_obj = None
         self.pincell_obj = None
+        self.union_obj = None            # UnionizedIndex on the device (set_accel)
+        self.union_merged = False
         self.n_bins = 0
         self.max_comp = 0
         self.n_materials = 0
@@ -82,6 +84,8 @@ class DeviceEngine:
                             arrs[8].shape[0], *[N.ptr(a) for a in arrs], float(emin), float(emax))
         N.check(self.lib.emc_upload_library(self._h, C.byref(desc)), "emc_upload_library")
         self.library_obj = weakref.ref(library)
+        self.union_obj = None            # the upload dropped the union index
+        self.union_merged = False
         self.n_materials = arrs[7].shape[0] - 1
         self.max_comp = int(np.max(np.diff(arrs[7]))) if self.n_materials else 0
 
@@ -192,6 +196,26 @@ class DeviceEngine:
         if parts is not None and self.max_comp == 0:
             parts = parts[:, :0]
         return sums, parts
+
+    ACCEL_CODES = {"binary": 0, "double_index": 1, "unionized": 2}
+
+    def set_accel(self, accel: str, index=None) -> None:
+        """Lookup backend (kernels.py ACCEL_*): "binary" = the device's log-hash
+        search; "double_index" / "unionized" = the union grid of `index`
+        (uploaded once per index object), merged channels for "unionized"."""
+        code = self.ACCEL_CODES[accel]
+        if code and (self.union_obj is None or self.union_obj() is not index or
+                     (code == 2 and not self.union_merged)):
+            ug = np.ascontiguousarray(index.union_grid, np.float64)
+            mp = np.ascontiguousarray(index.index_map, np.int32)
+            mg = None
+            if code == 2:
+                mg = np.ascontiguousarray(index.merged_channels, np.float64)
+            N.check(self.lib.emc_upload_union(self._h, N.ptr(ug), ug.shape[0], N.ptr(mp),
+                                              N.ptr(mg) if mg is not None else None), "emc_upload_union")
+            self.union_obj = weakref.ref(index)
+            self.union_merged = mg is not None
+        N.check(self.lib.emc_set_accel(self._h, code), "emc_set_accel")
 
     def grid_index(self, entries: np.ndarray, ens: np.ndarray) -> np.ndarray:
         """[n, 2] (clamp state, bracket index) of composition entries at E."""

@@ -115,23 +115,33 @@ def run_replicated(config: RunConfig, library, pincell, index=None, *,
         if mid < 0 or mid >= library.n_materials:
             raise ConfigurationError(f"geometry references material {mid} "
                                      f"but the library has {library.n_materials}")
-    if config.accel != "binary" and index is not None and config.accel == "unionized" \
-            and index.merged_channels is None:
-        xslib.merge_channels(library, index)   # API parity (R:145-152); device search is log-hashed
+    index = _union_for(config, library, index)
 
     world = current_world()
     if world.distributed:
         if devices is not None:
             raise ConfigurationError("devices= is for single-process runs; under "
                                      "torch.distributed each rank uses its own GPU")
-        return _run_rank(config, library, pincell, world, on_batch)
+        return _run_rank(config, library, pincell, world, on_batch, index=index)
     devs = resolve_devices(config, devices)
     if len(devs) == 1:
-        return _run_rank(config, library, pincell, World(device=devs[0]), on_batch)
-    return _run_threads(config, library, pincell, devs, on_batch)
+        return _run_rank(config, library, pincell, World(device=devs[0]), on_batch, index=index)
+    return _run_threads(config, library, pincell, devs, on_batch, index)
 
 
-def _run_threads(config, library, pincell, devs, on_batch) -> RunResult:
+def _union_for(config: RunConfig, library, index):
+    """R:145-152: the union index the lookup backend needs (built when not
+    given; merged channels materialized for "unionized"); None for binary."""
+    if config.accel == "binary":
+        return None
+    if index is None:
+        index = xslib.build_unionized_index(library)
+    if config.accel == "unionized" and index.merged_channels is None:
+        xslib.merge_channels(library, index)
+    return index
+
+
+def _run_threads(config, library, pincell, devs, on_batch, index=None) -> RunResult:
     import threading
 
     import torch
@@ -150,7 +160,7 @@ def _run_threads(config, library, pincell, devs, on_batch) -> RunResult:
             torch.cuda.set_device(devs[r])
             w = World(rank=r, size=len(devs), device_backend=True, group=group, device=devs[r])
             results[r] = _run_rank(config, library, pincell, w, on_batch if r == 0 else None,
-                                   slot=slots[r])
+                                   slot=slots[r], index=index)
         except BaseException as e:  # noqa: BLE001
             errors[r] = e
             group.abort()
@@ -168,7 +178,8 @@ def _run_threads(config, library, pincell, devs, on_batch) -> RunResult:
     return results[0]
 
 
-def _run_rank(config: RunConfig, library, pincell, world: World, on_batch, slot: int = 0) -> RunResult:
+def _run_rank(config: RunConfig, library, pincell, world: World, on_batch, slot: int = 0,
+              index=None) -> RunResult:
     """One rank's share of run_replicated; the returned RunResult is complete
     on rank 0 (global k, tallies, counters, final bank)."""
     ppb = config.particles_per_batch
@@ -176,6 +187,7 @@ def _run_rank(config: RunConfig, library, pincell, world: World, on_batch, slot:
         raise ConfigurationError("more ranks than particles per batch")
     g_lo, g_hi = block_of(world.rank, world.size, ppb)
     eng = engine_for(_local_device(world), library, pincell, slot)
+    eng.set_accel(config.accel, index)
     eng.set_extensions(pincell, config)
     eng.configure(config, g_lo, g_hi - g_lo)
     fixed_source = config.run_mode == "fixed_source"

@@ -319,9 +319,11 @@ def _check_energy(energy: float) -> None:
 
 
 def macro_lookup_batch(library: Library, material_ids, energies,
-                       partials: bool = True):
+                       partials: bool = True, accel: str = "binary",
+                       index: UnionizedIndex | None = None):
     """Vectorised macro_lookup on the GPU: returns (sums[n,5] =
-    (t, s, c, f, nu_f), partials[n, max_comp, 4] or None)."""
+    (t, s, c, f, nu_f), partials[n, max_comp, 4] or None).  `accel` selects
+    the lookup backend (K:306-320); the union ones need `index`."""
     from .engine import api_engine
     mats = np.ascontiguousarray(material_ids, np.int32)
     ens = np.ascontiguousarray(energies, np.float64)
@@ -331,7 +333,18 @@ def macro_lookup_batch(library: Library, material_ids, energies,
         raise UnknownMaterialError("material id not in library")
     if ens.size and not (np.all(np.isfinite(ens)) and np.all(ens > 0.0)):
         raise InvalidEnergyError("lookup energies must be finite and positive")
-    return api_engine(library=library).xs_lookup(mats, ens, partials)
+    if accel not in ACCEL_CODES:
+        raise ConfigurationError(f"unknown lookup backend {accel!r}")
+    if accel != "binary" and index is None:
+        raise ConfigurationError(f"accel={accel!r} requires a UnionizedIndex")
+    if accel == "unionized" and index.merged_channels is None:
+        merge_channels(library, index)
+    eng = api_engine(library=library)
+    eng.set_accel(accel, index)
+    try:
+        return eng.xs_lookup(mats, ens, partials)
+    finally:
+        eng.set_accel("binary")
 
 
 def macro_lookup(library: Library, material_id: int, energy: float,
@@ -350,7 +363,7 @@ def macro_lookup(library: Library, material_id: int, energy: float,
         if accel == "unionized" and index.merged_channels is None:
             merge_channels(library, index)
     ncomp = len(library.materials[material_id].composition)
-    sums, parts = macro_lookup_batch(library, [material_id], [energy])
+    sums, parts = macro_lookup_batch(library, [material_id], [energy], accel=accel, index=index)
     return MacroXS(*(float(v) for v in sums[0])), parts[0, :ncomp].copy()
 
 

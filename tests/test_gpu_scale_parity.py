@@ -123,3 +123,41 @@ def test_scale_run_matches_oracle(problem, tail_n, c3, c4, engine_env):
     assert res.physics_fingerprint() == want
     for k in ("events_lookup", "events_advance", "events_collision", "fissions", "captures"):
         assert res.counters[k] == ores["counters"][k], k
+
+
+@pytest.fixture(scope="module")
+def c3_index(c3):
+    lib, _ = c3
+    return P.build_unionized_index(lib, merged=True)
+
+
+def test_union_backends_criterion4_c3(c3, c3_index):
+    """The reference's criterion 4 (tests/test_acceptance.py:122-148) on the
+    device: 10^5 random (material, E) queries give bit-identical sums and
+    partials through the three lookup backends (log-hash for "binary", union
+    grid + bracket map for "double_index", + merged channels for "unionized")."""
+    lib, _ = c3
+    rng = np.random.RandomState(11)
+    n = 10**5
+    E = np.exp(rng.uniform(np.log(1e-6), np.log(3e7), n))
+    E[:4] = [c3_index.union_grid[0], c3_index.union_grid[-1], c3_index.union_grid[1], c3_index.union_grid[-2]]
+    mats = rng.randint(0, lib.n_materials, n)
+    ref = P.xslib.macro_lookup_batch(lib, mats, E)
+    for accel in ("double_index", "unionized"):
+        got = P.xslib.macro_lookup_batch(lib, mats, E, accel=accel, index=c3_index)
+        assert np.array_equal(got[0], ref[0]), accel
+        assert np.array_equal(got[1], ref[1]), accel
+
+
+@pytest.mark.parametrize("accel", ["double_index", "unionized"])
+def test_union_backend_run_matches_oracle(accel, c3, c3_index):
+    """Transport with the union-grid lookup kernels (k_lookup_union) on the C3
+    library, 300k in flight: the oracle's (binary-search) fingerprint."""
+    lib, cell = c3
+    cfg = P.RunConfig(particles_per_batch=300_000, inactive_batches=1, active_batches=2,
+                      mode="event", seed=42, max_in_flight=300_000, reduction="deterministic")
+    if "c3" not in _ORACLE:
+        _ORACLE["c3"] = _oracle_fingerprint(lib, cell, cfg)
+    want, _ = _ORACLE["c3"]
+    res = P.run_replicated(P.RunConfig(**dict(cfg.__dict__, accel=accel)), lib, cell, index=c3_index)
+    assert res.physics_fingerprint() == want
