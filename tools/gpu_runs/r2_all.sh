@@ -1,0 +1,12 @@
+#!/bin/bash
+# round 2 checkpoint: smoke + every workload's bench line (driver shape 5+20) + reference arm + launch list
+mkdir -p gpurun_out
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+for w in c4 c4pin c3 c3pin c2 c1 c5; do
+  timeout 900 python bench.py --workload $w 2>&1 | grep '^{' | tail -1 > gpurun_out/r2c_bench_$w.json
+  python -c "import json; d=json.load(open('gpurun_out/r2c_bench_$w.json')); r=d['roofline']; print('$w', round(d['value']/1e6,3), 'M/s e2e', round(d['e2e']['value']/1e6,3), 'cpu', (d.get('cpu_baseline') or {}).get('value'), 'l1frac', r.get('frac'), d['clocks'])"
+done
+timeout 900 python bench.py --impl reference 2>&1 | grep '^{' | tail -1 > gpurun_out/r2c_bench_reference.json
+python -c "import json; d=json.load(open('gpurun_out/r2c_bench_reference.json')); print('reference', d['value'], d['cpu_baseline'])"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2c_launches.csv python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-counters > /dev/null 2>&1
+echo done
