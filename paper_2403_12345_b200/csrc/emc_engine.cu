@@ -154,6 +154,7 @@ struct emc_ctx {
     bool lk_piped = true;        // chunk-pipelined staged lookup on sorted queues (EMC_LK_PIPED)
     int lk_pcfg = 1;             // its CTA configuration (EMC_LK_PCFG: 0 = 32 warps x 1, 1 = 16 warps x 2, 2 = 10 x 3)
     DSlots S{};
+    bool ck_pmajor = false;      // sigma_t checkpoints particle-major (EMC_CK_PMAJOR)
 
     // queues + sort scratch
     DBuf<int32_t> qa, qb, qs, qc, qx;
@@ -191,8 +192,9 @@ struct emc_ctx {
     int64_t tail_sub_n = 131072; // ... up to this length 8 lanes per particle (EMC_TAIL_SUB_N)
     bool all_small = false;      // no composition group is staged (all < LK_MIN_NUC): the gather kernel serves
     // small-population finish (EMC_FINISH_N): a tail queue at most this long is
-    // carried to death by k_finish (one thread per particle) in one launch;
-    // -1 = by library (whole tail for gather-lookup libraries, off for staged ones)
+    // carried to death in one launch (k_finish: one thread per particle for
+    // gather-lookup libraries; k_finish_warp: one warp per particle for staged
+    // ones); -1 = by library (whole tail / 32768)
     int64_t finish_n = -1;
     cudaEvent_t evt[4 * 32]{};
     bool ev_init = false;
@@ -558,7 +560,12 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
     c->reorder = !(ro && ro[0] == '0');
     if (c->reorder) rc |= c->ps2.alloc(nslots);
     rc |= c->iota.alloc(nslots);
-    rc |= c->ckpt.alloc(std::max<int64_t>(1, (int64_t)c->nck * nslots));
+    // sigma_t checkpoint layout (DSlots): row-major [nck][nslots] or, with
+    // EMC_CK_PMAJOR=1, particle-major [nslots][nck rounded up to 4] (32-byte rows)
+    const char* pm = getenv("EMC_CK_PMAJOR");
+    c->ck_pmajor = pm && pm[0] == '1';
+    const int64_t nck_pad = c->ck_pmajor ? ((int64_t)c->nck + 3) / 4 * 4 : c->nck;
+    rc |= c->ckpt.alloc(std::max<int64_t>(1, nck_pad * nslots));
     for (auto* b : {&c->qa, &c->qb, &c->qs, &c->qc, &c->qx})
         rc |= b->alloc(nslots);
     rc |= c->keys_in.alloc(nslots); rc |= c->keys_out.alloc(nslots); rc |= c->keys_b.alloc(nslots);
@@ -571,7 +578,8 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
         EMC_TRY_CUDA(cudaMemcpy(c->iota.p, h.data(), nslots * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
     c->ps_cur = c->ps.p;
-    c->S = DSlots{c->ps_cur, c->ckpt.p, nslots, c->nck};
+    c->S = DSlots{c->ps_cur, c->ckpt.p, nslots, c->nck, c->ck_pmajor ? (int32_t)nck_pad : 1,
+                  c->ck_pmajor ? (int64_t)1 : nslots};
     // fission bank: reference starts at n_assigned*6+1024 (R:92); ~1 site per
     // source particle is typical, so start at 2x and grow on overflow.
     if ((rc = alloc_sites(c, (size_t)(cfg->n_assigned * 2 + 4096)))) return rc;
@@ -800,12 +808,16 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
         int64_t look_inv = 0, tail_blocks = 0;
         float ms;
         while (nL > 0 && c->ctl_host->err == 0) {
-            const int64_t fin_n = c->finish_n >= 0 ? c->finish_n : (c->all_small ? c->tail_n : 0);
+            const int64_t fin_n = c->finish_n >= 0 ? c->finish_n : (c->all_small ? c->tail_n : 32768);
             if (nL <= fin_n && c->ctl_host->cursor >= (unsigned long long)cf.n_assigned) {
                 // small population: finish every remaining history in one launch
                 EMC_TRY_CUDA(cudaEventRecord(c->ev[0], st));
-                k_finish<<<(unsigned)((nL + 127) / 128), 128, 0, st>>>(cur, nL, bp, c->L, c->G, c->S, lg, sv,
-                                                                       c->bins.p, c->ctl.p, c->cnt.p, c->M);
+                if (c->all_small)     // gather-lookup library: one thread per particle
+                    k_finish<<<(unsigned)((nL + 127) / 128), 128, 0, st>>>(cur, nL, bp, c->L, c->G, c->S, lg, sv,
+                                                                           c->bins.p, c->ctl.p, c->cnt.p, c->M);
+                else                  // staged library: one warp per particle (warp-cooperative lookups)
+                    k_finish_warp<<<(unsigned)std::min<int64_t>((nL + 3) / 4, (int64_t)c->sm_count * 16), 128, 0,
+                                    st>>>(cur, nL, bp, c->L, c->G, c->S, lg, sv, c->bins.p, c->ctl.p, c->cnt.p, c->M);
                 EMC_CHECK_LAUNCH(c);
                 EMC_TRY_CUDA(cudaEventRecord(c->ev[1], st));
                 EMC_TRY_CUDA(cudaMemsetAsync(&c->ctl.p->nL2, 0, sizeof(unsigned), st));

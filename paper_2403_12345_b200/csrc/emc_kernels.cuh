@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_lookup(const int32_t* __restr
             double E = S.ps[s].a.E;
             int32_t m = S.ps[s].d.mat;
             P2 c;
-            macro_tcf(L, m, E, c.t, c.c, c.f, c.nsf, fused ? S.ckpt + s : nullptr, S.nck, S.nslots);
+            macro_tcf(L, m, E, c.t, c.c, c.f, c.nsf, fused ? ckpt_of(S, s) : nullptr, S.nck, S.ck_row);
             S.ps[s].c = c;
             nl += (unsigned long long)(__ldg(L.mat_off + m + 1) - __ldg(L.mat_off + m));
         }
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(256) k_lookup_union(const int32_t* __restrict_
             double E = S.ps[s].a.E;
             int32_t m = S.ps[s].d.mat;
             P2 c;
-            macro_tcf_union<MERGED>(L, U, m, E, c.t, c.c, c.f, c.nsf, fused ? S.ckpt + s : nullptr, S.nck, S.nslots);
+            macro_tcf_union<MERGED>(L, U, m, E, c.t, c.c, c.f, c.nsf, fused ? ckpt_of(S, s) : nullptr, S.nck, S.ck_row);
             S.ps[s].c = c;
             nl += (unsigned long long)(__ldg(L.mat_off + m + 1) - __ldg(L.mat_off + m));
         }
@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(256) k_lookup_warp(const int32_t* __restrict__
         }
         int32_t nmax = ncomp;
         for (int o = 16; o; o >>= 1) nmax = max(nmax, __shfl_xor_sync(kFull, nmax, o));
-        double* const ck = (fused && have) ? S.ckpt + s : nullptr;
+        double* const ck = (fused && have) ? ckpt_of(S, s) : nullptr;
         double st = 0.0, sc = 0.0, sf = 0.0, snf = 0.0;
         for (int32_t k0 = 0; k0 < nmax; k0 += LPP) {
             double t = 0.0, cc = 0.0, f = 0.0, den = 0.0, dn = 0.0;
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(256) k_lookup_warp(const int32_t* __restrict__
                     snf = __dadd_rn(snf, __dmul_rn(dnj, fj));
                     if (ck && sub == 0 && ((k0 + j + 1) & (kCkptStride - 1)) == 0) {
                         const int32_t row = (k0 + j + 1) / kCkptStride - 1;
-                        if (row < S.nck) ck[(int64_t)row * S.nslots] = st;
+                        if (row < S.nck) ck[(int64_t)row * S.ck_row] = st;
                     }
                 }
             }
@@ -745,7 +745,7 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_collision(const int32_t* 
             double u1 = draw(b.rng, d.draws);
             double tgt = __dmul_rn(u1, st);
             double pt_sel;
-            int32_t ksel = select_nuclide(L, S.ckpt + s, S.nck, S.nslots, e0, e1, bin, E, tgt,
+            int32_t ksel = select_nuclide(L, ckpt_of(S, s), S.nck, S.ck_row, e0, e1, bin, E, tgt,
                                           bp.fused != 0, pt_sel, interp);
             const Comp cs = L.comp[ksel];
             double s_s, s_c, s_f;

@@ -361,13 +361,13 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         // done right here, lane by lane, without the block-wide pass machinery
         {
             const bool ckon0 = MODE == 1 || fused;
-            const int64_t cks0 = MODE == 0 ? S.nslots : (int64_t)n;
+            const int64_t cks0 = MODE == 0 ? S.ck_row : (int64_t)n;
 #pragma unroll
             for (int p = 0; p < PPL; ++p) {
                 if (pend[p] && __ldg(L.grp_off + grp[p] + 1) - __ldg(L.grp_off + grp[p]) < LK_MIN_NUC) {
                     double t0, c0, f0, n0;
                     macro_tcf(L, m[p], E[p], t0, c0, f0, n0,
-                              ckon0 ? (MODE == 0 ? S.ckpt + s[p] : bout + n + i[p]) : nullptr, nck, cks0);
+                              ckon0 ? (MODE == 0 ? ckpt_of(S, s[p]) : bout + n + i[p]) : nullptr, nck, cks0);
                     if (MODE == 0) {
                         P2 c; c.t = t0; c.c = c0; c.f = f0; c.nsf = n0;
                         (rdst ? rdst : S.ps)[s[p]].c = c;
@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
             // sigma_t checkpoints: row r of particle p at ckb[r * cks] (formed at
             // the store, not kept live through the nuclide loop)
             const bool ckon = MODE == 1 || fused;
-            const int64_t cks = MODE == 0 ? S.nslots : (int64_t)n;
+            const int64_t cks = MODE == 0 ? S.ck_row : (int64_t)n;
             const int nst = (ncomp + LK_G - 1) / LK_G;
 
             if (ncomp < LK_MIN_NUC) {
@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                 for (int p = 0; p < PPL; ++p)
                     if (mine[p])
                         macro_tcf(L, m[p], E[p], st[p], sc[p], sf[p], snf[p],
-                                  ckon ? (MODE == 0 ? S.ckpt + s[p] : bout + n + i[p]) : nullptr, nck, cks);
+                                  ckon ? (MODE == 0 ? ckpt_of(S, s[p]) : bout + n + i[p]) : nullptr, nck, cks);
             } else if (producer) {
                 // lane j < LK_G owns nuclide 8t+j of every stage; its global
                 // reads for stage t+1 are issued before it waits for slot t
@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                             const int32_t row = (t + 1) / CKS - 1;
 #pragma unroll
                             for (int p = 0; p < PPL; ++p) {
-                                double* ckb = MODE == 0 ? S.ckpt + s[p] : bout + n + i[p];
+                                double* ckb = MODE == 0 ? ckpt_of(S, s[p]) : bout + n + i[p];
                                 if (mine[p] && row < nck) ckb[(int64_t)row * cks] = st[p];
                             }
                         }
@@ -602,7 +602,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
     const bool producer = warp == LK_CONS;
     const int32_t nck = MODE == 0 ? S.nck : 16;
     const bool ckon = MODE == 1 || fused;
-    const int64_t cks = MODE == 0 ? S.nslots : (int64_t)n;
+    const int64_t cks = MODE == 0 ? S.ck_row : (int64_t)n;
 
     if (threadIdx.x == 0) {
         for (int d = 0; d < LK_D; ++d) {
@@ -728,7 +728,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
         if (pend && pidx < 0) {
             // not covered by a pass: small group (the moderator) or an odd chunk
             double t0, c0, f0, n0;
-            macro_tcf(L, m, E, t0, c0, f0, n0, ckon ? (MODE == 0 ? S.ckpt + s : bout + n + i) : nullptr, nck, cks);
+            macro_tcf(L, m, E, t0, c0, f0, n0, ckon ? (MODE == 0 ? ckpt_of(S, s) : bout + n + i) : nullptr, nck, cks);
             if (MODE == 0) {
                 P2 cc; cc.t = t0; cc.c = c0; cc.f = f0; cc.nsf = n0;
                 (rdst ? rdst : S.ps)[s].c = cc;
@@ -825,7 +825,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                     constexpr int CKS = kCkptStride / LK_G;
                     if (ckon && (t + 1) % CKS == 0 && (t + 1) * LK_G <= ncomp) {
                         const int32_t row = (t + 1) / CKS - 1;
-                        double* ckb = MODE == 0 ? S.ckpt + s : bout + n + i;
+                        double* ckb = MODE == 0 ? ckpt_of(S, s) : bout + n + i;
                         if (mine && row < nck) ckb[(int64_t)row * cks] = st;
                     }
                 }

@@ -185,13 +185,16 @@ def _edge_library():
     return lib, cell
 
 
-@pytest.mark.parametrize("cap,tail_n", [(3000, 0), (3000, None), (256, 0), (256, None)])
+@pytest.mark.parametrize("cap,tail_n", [(3000, 0), (3000, None), (256, 0), (256, None), (3000, "finish")])
 def test_edge_library_staged_paths_match_oracle(cap, tail_n, engine_env):
-    """tail_n=0 disables tail mode, so every sweep is sorted and goes through the
-    staged kernels (with cap = ppb the default threshold would put the whole
-    run in tail mode, served by the warp-per-particle kernel)."""
-    if tail_n is not None:
-        engine_env(EMC_TAIL_N=tail_n)
+    """tail_n=0 disables tail mode and the finish, so every sweep is sorted and
+    goes through the staged kernels (with cap = ppb the default thresholds
+    would hand the whole run to the finish / tail kernels); "finish" runs every
+    batch through k_finish_warp."""
+    if tail_n == "finish":
+        engine_env(EMC_FINISH_N=100_000_000)
+    elif tail_n is not None:
+        engine_env(EMC_TAIL_N=tail_n, EMC_FINISH_N=0)
     lib, cell = _edge_library()
     cfg = P.RunConfig(particles_per_batch=3000, inactive_batches=2, active_batches=2, mode="event",
                       reduction="deterministic", max_in_flight=cap)

@@ -104,21 +104,25 @@ _ORACLE = {}
 
 
 @pytest.mark.parametrize("problem", ["c3", "c4"])
-@pytest.mark.parametrize("tail_n", [None, "4096"])
+@pytest.mark.parametrize("tail_n", [None, "4096", "finish"])
 def test_scale_run_matches_oracle(problem, tail_n, c3, c4, engine_env):
     """300k particles per batch, all in flight (1 inactive + 2 active batches,
     deterministic reduction): sorted sweeps of >= 262k particles go through the
-    pipelined staged lookup; with EMC_TAIL_N=4096 every sweep down to 4096
-    particles does.  Fingerprint (k series, tallies, banks, event counts) must
-    equal the oracle's."""
+    pipelined staged lookup; with EMC_TAIL_N=4096 (finish off) every sweep down
+    to 4096 particles does; "finish" hands every whole batch to the
+    warp-cooperative finish kernel (k_finish_warp) right after sourcing.
+    Fingerprint (k series, tallies, banks, event counts) must equal the
+    oracle's."""
     lib, cell = c3 if problem == "c3" else c4
     cfg = P.RunConfig(particles_per_batch=300_000, inactive_batches=1, active_batches=2,
                       mode="event", seed=42, max_in_flight=300_000, reduction="deterministic")
     if problem not in _ORACLE:
         _ORACLE[problem] = _oracle_fingerprint(lib, cell, cfg)
     want, ores = _ORACLE[problem]
-    if tail_n is not None:
-        engine_env(EMC_TAIL_N=tail_n)
+    if tail_n == "finish":
+        engine_env(EMC_FINISH_N=100_000_000)
+    elif tail_n is not None:
+        engine_env(EMC_TAIL_N=tail_n, EMC_FINISH_N=0)
     res = P.run_replicated(cfg, lib, cell)
     assert res.physics_fingerprint() == want
     for k in ("events_lookup", "events_advance", "events_collision", "fissions", "captures"):
