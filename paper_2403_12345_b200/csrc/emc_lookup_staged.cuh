@@ -27,6 +27,10 @@ namespace emc {
 // CTA = NW warps: NW-1 consumer warps (one particle per lane; a chunk is
 // (NW-1)*32 consecutive queue entries) + 1 producer warp; MINB CTAs per SM.
 constexpr int LK_G = 8;                    // nuclides per pipeline stage
+#ifndef EMC_LK_FAST_UNROLL
+#define EMC_LK_FAST_UNROLL 8
+#endif
+constexpr int kLkFastUnroll = EMC_LK_FAST_UNROLL;   // unroll of the stage fast path's nuclide loop
 #ifndef EMC_LK_D
 #define EMC_LK_D 3
 #endif
@@ -770,7 +774,7 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                         const longlong2 ab = sh.hdr[d][j];
                         lis |= ((uint32_t)(ab.x <= Eb) + (uint32_t)(ab.y <= Eb)) << (2 * j);
                     }
-#pragma unroll
+#pragma unroll kLkFastUnroll
                     for (int j = 0; j < LK_G; ++j) {
                         const int k = t * LK_G + j;
                         const int32_t li = (int32_t)((lis >> (2 * j)) & 3u);
