@@ -175,6 +175,9 @@ struct emc_ctx {
     int64_t log_n = 0;
     size_t log_want = 0;                  // capacity the next batch's log needs (presize_logs)
     DBuf<uint64_t> lkey_in, lkey_out; DBuf<double> lval_out;
+    // the sorted log: CUB double-buffer mode ping-pongs (lkey_in, lkey_out) and
+    // (lg_val, lval_out), so its scratch stays small at > 2^31 entries
+    const uint64_t* lkey_sorted = nullptr; const double* lval_sorted = nullptr;
     int gid_bits = 1;
 
     // per batch
@@ -635,9 +638,11 @@ extern "C" int emc_configure(emc_ctx* c, const emc_run_config* cfg)
                                     (int32_t*)nullptr, (int)std::max<int64_t>(nslots, scap), 0, 32);
     cub::DeviceRadixSort::SortPairs(nullptr, t2, (uint64_t*)nullptr, (uint64_t*)nullptr, (int32_t*)nullptr,
                                     (int32_t*)nullptr, (int)scap, 0, 64);
-    if (cfg->use_logs)
-        cub::DeviceRadixSort::SortPairs(nullptr, t3, (uint64_t*)nullptr, (uint64_t*)nullptr, (double*)nullptr,
-                                        (double*)nullptr, (int64_t)c->lg_gid.n, 0, 64);
+    if (cfg->use_logs) {
+        cub::DoubleBuffer<uint64_t> dk(nullptr, nullptr);
+        cub::DoubleBuffer<double> dv(nullptr, nullptr);
+        cub::DeviceRadixSort::SortPairs(nullptr, t3, dk, dv, (int64_t)c->lg_gid.n, 0, 64);
+    }
     if (c->cub_tmp.alloc(std::max<size_t>(std::max(t1, std::max(t2, t3)), 1))) return EMC_E_OOM;
     c->bank_n = 0;
     c->src = DSrc{nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, 0.0, 0};
@@ -716,12 +721,18 @@ static int presize_logs(emc_ctx* c)
 {
     const size_t want = c->log_want;
     if (!c->cfg.use_logs || want <= c->lg_gid.n) return 0;
+    // only when the larger log fits next to everything else (48 B per entry);
+    // otherwise keep the current one: the next batch grows-and-reruns if needed
+    size_t free_b = 0, total_b = 0;
+    EMC_TRY_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    if ((want - c->lg_gid.n) * 48 + ((size_t)1 << 30) > free_b) return 0;
     c->lg_gid.release(); c->lg_ord.release(); c->lg_bin.release(); c->lg_val.release();
     c->lkey_in.release(); c->lkey_out.release(); c->lval_out.release();
     if (int rc = alloc_logs(c, want)) return rc;
     size_t need = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, need, c->lkey_in.p, c->lkey_out.p, c->lg_val.p, c->lval_out.p,
-                                    (int64_t)want, 0, 64, c->stream);
+    cub::DoubleBuffer<uint64_t> dk(c->lkey_in.p, c->lkey_out.p);
+    cub::DoubleBuffer<double> dv(c->lg_val.p, c->lval_out.p);
+    cub::DeviceRadixSort::SortPairs(nullptr, need, dk, dv, (int64_t)want, 0, 64, c->stream);
     if (need > c->cub_tmp.n && c->cub_tmp.alloc(need)) return EMC_E_OOM;
     return 0;
 }
@@ -1110,15 +1121,27 @@ extern "C" int emc_run_batch(emc_ctx* c, const emc_batch_args* a, emc_batch_resu
     c->bank_n = n;
     // deterministic mode: sort the log by (bin, gid, ordinal) now
     c->log_n = res->n_logs;
+    c->lkey_sorted = c->lkey_out.p;
+    c->lval_sorted = c->lval_out.p;
     if (c->cfg.use_logs && c->log_n > 0) {
         k_log_keys<<<grid_for(c->log_n, 256, 1 << 30), 256, 0, st>>>(c->lg_gid.p, c->lg_ord.p, c->lg_bin.p,
                                                                      c->log_n, c->cfg.gid_lo, c->gid_bits,
                                                                      c->lkey_in.p);
         EMC_CHECK_LAUNCH(c);
         int bb = bits_for(c->n_bins);
-        int rc = sort_cub64(c, c->lkey_in.p, c->lkey_out.p, c->lg_val.p, c->lval_out.p, c->log_n,
-                            bb + c->gid_bits + 17);
-        if (rc) return rc;
+        {
+            cub::DoubleBuffer<uint64_t> dk(c->lkey_in.p, c->lkey_out.p);
+            cub::DoubleBuffer<double> dv(c->lg_val.p, c->lval_out.p);
+            size_t need = 0;
+            const int end_bit = bb + c->gid_bits + 17;
+            cub::DeviceRadixSort::SortPairs(nullptr, need, dk, dv, (int64_t)c->log_n, 0, end_bit, st);
+            if (need > c->cub_tmp.n && c->cub_tmp.alloc(need)) return EMC_E_OOM;
+            EMC_TRY_CUDA(cub::DeviceRadixSort::SortPairs(c->cub_tmp.p, need, dk, dv, (int64_t)c->log_n, 0, end_bit,
+                                                         st));
+            c->launches += (end_bit + 7) / 8;
+            c->lkey_sorted = dk.Current();
+            c->lval_sorted = dv.Current();
+        }
     }
     EMC_TRY_CUDA(cudaStreamSynchronize(st));
     res->launches = c->launches - l0;
@@ -1134,7 +1157,7 @@ extern "C" int emc_reduce_bins(emc_ctx* c, const double* init, double* out, int6
     else EMC_TRY_CUDA(cudaMemsetAsync(c->bins_init.p, 0, n_bins * 8, st));
     if (c->cfg.use_logs) {
         if (c->trace) EMC_TRY_CUDA(cudaEventRecord(c->ev[7], st));
-        k_log_fold<<<(unsigned)n_bins, LF_THREADS, 0, st>>>(c->lkey_out.p, c->lval_out.p, c->log_n,
+        k_log_fold<<<(unsigned)n_bins, LF_THREADS, 0, st>>>(c->lkey_sorted, c->lval_sorted, c->log_n,
                                                                     c->gid_bits + 17, (int32_t)n_bins,
                                                                     c->bins_init.p, c->bins_out.p);
         EMC_CHECK_LAUNCH(c);

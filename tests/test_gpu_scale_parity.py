@@ -165,3 +165,36 @@ def test_union_backend_run_matches_oracle(accel, c3, c3_index):
     want, _ = _ORACLE["c3"]
     res = P.run_replicated(P.RunConfig(**dict(cfg.__dict__, accel=accel)), lib, cell, index=c3_index)
     assert res.physics_fingerprint() == want
+
+
+@pytest.mark.slow
+def test_deterministic_log_above_int32(engine_env):
+    """the deterministic contribution log passes 2^31 entries
+    around 13-14M histories per rank (~160 entries per history on this
+    library).  One scored 14M-particle batch: the log holds > 2^31 entries,
+    is sorted with 64-bit item counts and folded; its bins equal the fast
+    (atomic) sums of the same batch to 1e-9 relative (same histories: k_run =
+    1 in batch 0; only the summation order differs)."""
+    from paper_2403_12345_b200.engine import DeviceEngine
+    lib, cell = P.depleted_pincell(12, 3, 100, 8, seed=1)
+    ppb = 14_000_000
+    out = {}
+    for red in ("deterministic", "fast"):
+        eng = DeviceEngine(0)
+        try:
+            eng.upload_library(lib)
+            eng.upload_geometry(cell)
+            cfg = P.RunConfig(particles_per_batch=ppb, inactive_batches=0, active_batches=1, mode="event",
+                              seed=42, max_in_flight=ppb, reduction=red)
+            eng.set_extensions(cell, cfg)
+            eng.configure(cfg, 0, ppb)
+            res = eng.run_batch(0, 1.0, batch0=True, score=True)
+            assert res.error == 0
+            out[red] = (res, eng.reduce_bins(None))
+        finally:
+            eng.close()
+    det, fast = out["deterministic"], out["fast"]
+    assert det[0].n_logs > 2**31
+    assert det[0].n_sites == fast[0].n_sites
+    assert np.allclose(det[1], fast[1], rtol=1e-9, atol=0)
+    assert det[1][-1] > 0.0
