@@ -823,9 +823,11 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             if (nL <= fin_n && c->ctl_host->cursor >= (unsigned long long)cf.n_assigned) {
                 // small population: finish every remaining history in one launch
                 EMC_TRY_CUDA(cudaEventRecord(c->ev[0], st));
-                if (c->all_small)     // gather-lookup library: one thread per particle
-                    k_finish<<<(unsigned)((nL + 127) / 128), 128, 0, st>>>(cur, nL, bp, c->L, c->G, c->S, lg, sv,
-                                                                           c->bins.p, c->ctl.p, c->cnt.p, c->M);
+                if (c->all_small) {   // gather-lookup library: one thread per particle, spread over the SMs
+                    const int fb = nL <= 64LL * c->sm_count ? 32 : nL <= 128LL * c->sm_count ? 64 : 128;
+                    k_finish<<<(unsigned)((nL + fb - 1) / fb), fb, 0, st>>>(cur, nL, bp, c->L, c->G, c->S, lg, sv,
+                                                                            c->bins.p, c->ctl.p, c->cnt.p, c->M);
+                }
                 else                  // staged library: one warp per particle (warp-cooperative lookups)
                     k_finish_warp<<<(unsigned)std::min<int64_t>((nL + 3) / 4, (int64_t)c->sm_count * 16), 128, 0,
                                     st>>>(cur, nL, bp, c->L, c->G, c->S, lg, sv, c->bins.p, c->ctl.p, c->cnt.p, c->M);
