@@ -126,7 +126,8 @@ def capture(particles: int, workload: str, sample=None, timeout: int = 900, log:
     log = log or os.path.join(ROOT, "gpurun_out", "lookup_counters.csv")
     os.makedirs(os.path.dirname(log), exist_ok=True)
     kern = "k_lookup_piped" if sample else "k_lookup_(piped|staged|warp)"
-    cmd = ["ncu", "--metrics", ",".join(METRICS), "-k", f"regex:{kern}", "--csv", "--log-file", log]
+    cmd = ["ncu", "--clock-control", "none", "--metrics", ",".join(METRICS), "-k", f"regex:{kern}", "--csv",
+           "--log-file", log]
     if sample:
         cmd += ["-s", str(sample[0]), "-c", str(sample[1])]
     cmd += [sys.executable, os.path.join(ROOT, "tools", "profile_step.py"), "--particles", str(particles),
