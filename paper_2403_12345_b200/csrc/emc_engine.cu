@@ -199,6 +199,7 @@ struct emc_ctx {
     // gather-lookup libraries; k_finish_warp: one warp per particle for staged
     // ones); -1 = by library (whole tail / 32768)
     int64_t finish_n = -1;
+    bool finish_warp = false;    // EMC_FINISH_WARP=1: warp-per-particle finish for gather-lookup libraries too
     cudaEvent_t evt[4 * 32]{};
     bool ev_init = false;
 };
@@ -231,6 +232,7 @@ extern "C" int emc_create(int device, emc_ctx** out)
     if (const char* t = getenv("EMC_TAIL_WARP_N")) c->tail_warp_n = std::max<int64_t>(0, atoll(t));
     if (const char* t = getenv("EMC_TAIL_SUB_N")) c->tail_sub_n = std::max<int64_t>(0, atoll(t));
     if (const char* t = getenv("EMC_FINISH_N")) c->finish_n = std::max<int64_t>(0, atoll(t));
+    if (const char* t = getenv("EMC_FINISH_WARP")) c->finish_warp = atoi(t) != 0;
     c->ev_init = true;
     *out = c;
     return 0;
@@ -823,7 +825,7 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
             if (nL <= fin_n && c->ctl_host->cursor >= (unsigned long long)cf.n_assigned) {
                 // small population: finish every remaining history in one launch
                 EMC_TRY_CUDA(cudaEventRecord(c->ev[0], st));
-                if (c->all_small) {   // gather-lookup library: one thread per particle, spread over the SMs
+                if (c->all_small && !c->finish_warp) {   // gather-lookup library: one thread per particle
                     const int fb = nL <= 64LL * c->sm_count ? 32 : nL <= 128LL * c->sm_count ? 64 : 128;
                     k_finish<<<(unsigned)((nL + fb - 1) / fb), fb, 0, st>>>(cur, nL, bp, c->L, c->G, c->S, lg, sv,
                                                                             c->bins.p, c->ctl.p, c->cnt.p, c->M);

@@ -32,6 +32,20 @@ namespace emc {
                  emc_stride_ = (int64_t)gridDim.x * blockDim.x;                            \
          emc_base_ < (int64_t)(n); emc_base_ += emc_stride_)
 
+// Prefetch the particle line this lane handles in the next grid-stride
+// iteration into L2, so its load there waits on L2 rather than DRAM.
+#ifndef EMC_PREFETCH
+#define EMC_PREFETCH 1
+#endif
+__device__ __forceinline__ void prefetch_next_line(const int32_t* __restrict__ q, int64_t i, int64_t stride,
+                                                   int64_t n, const PState* ps)
+{
+    if (EMC_PREFETCH && i + stride < n) {
+        const PState* p = ps + __ldg(q + i + stride);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+    }
+}
+
 // queue_push that also stores the lookup sort key at the pushed position
 __device__ __forceinline__ void queue_push_key(int32_t* q, unsigned int* count, int32_t slot, bool pred,
                                                uint32_t* keys, uint32_t key)
@@ -477,6 +491,7 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
         int64_t i = emc_base_ + lane_id();
         bool valid = i < n, to_col = false, to_cross = false, leak = false;
         int32_t s = valid ? q[i] : 0;
+        prefetch_next_line(q, i, emc_stride_, n, S.ps);
         double kE = 1.0;                     // energy for the next lookup's sort key
         P0 a{}; P1 b{}; P2 c{}; P3 d{};
         if (valid) {
