@@ -337,7 +337,10 @@ def run_reference(args):
     is Python/numba and cannot travel to the GPU box) on all host cores, in
     both of its executors (event: the reference default; history: CPU-optimal,
     PAPER.md:70); the line reports the faster one."""
-    rank, ws, _ = init_dist()
+    # CPU only: no process group (rank 0 works, the other ranks exit at once;
+    # an NCCL group the other ranks abandon could hang rank 0's exit)
+    rank = int(os.environ.get("RANK", "0"))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     lib, cell = problem(args)
