@@ -198,3 +198,48 @@ def test_deterministic_log_above_int32(engine_env):
     assert det[0].n_sites == fast[0].n_sites
     assert np.allclose(det[1], fast[1], rtol=1e-9, atol=0)
     assert det[1][-1] > 0.0
+
+
+@pytest.mark.slow
+def test_hm_core_10m_batch_matches_oracle():
+    """One 10M-history batch of the benchmark problem (C4 library on the HM
+    core, batch 0, deterministic reduction: ~1.6e9 log entries) against the
+    oracle's restatement run on all host cores: k, tallies, fission bank and
+    event counts bit for bit -- the full production path (sorted pipelined
+    sweeps at 10M in flight, same-material chains, tail, warp finish)."""
+    import os
+    from oracle import driver
+    lib, cell = P.hm_core(272, 3, 11303, 100, seed=1)
+    cfg = P.RunConfig(particles_per_batch=10_000_000, inactive_batches=1, active_batches=0, mode="event",
+                      seed=42, max_in_flight=10_000_000, reduction="deterministic")
+    res = P.run_replicated(cfg, lib, cell)
+    ores = driver.run(dict(cfg.__dict__, mode="history", lattice=(cell.lattice, cell.pitch, cell.pin_map)),
+                      lib.arrays(), cell.as_tuple(), workers=os.cpu_count() or 1)
+    assert res.physics_fingerprint() == driver.fingerprint(ores)
+    for k in ("events_lookup", "events_advance", "events_collision", "fissions", "captures", "interp_transport"):
+        assert res.counters[k] == ores["counters"][k], k
+
+
+@pytest.mark.slow
+def test_full_size_schedule_invariance_and_bank_order():
+    """Schedule invariance (the reference's acceptance criterion 1) at the
+    benchmark's full size: batch 0 of C4 on the HM core at 40M particles (k_run
+    = 1, so histories depend only on (seed, gid)) run with all particles in
+    flight and sorted lookups, and with a 10M in-flight cap, refills and
+    unsorted lookups: identical canonical fission banks and event counts; the
+    bank is in canonical (parent, ordinal) order."""
+    lib, cell = P.hm_core(272, 3, 11303, 100, seed=1)
+    out = []
+    for cap, srt in ((40_000_000, True), (10_000_000, False)):
+        cfg = P.RunConfig(particles_per_batch=40_000_000, inactive_batches=1, active_batches=0, mode="event",
+                          seed=42, max_in_flight=cap, sort_enabled=srt, reduction="fast")
+        out.append(P.run_replicated(cfg, lib, cell))
+    a, b = out
+    assert a.bank.tobytes() == b.bank.tobytes()
+    for k in ("events_lookup", "events_advance", "events_collision", "fissions", "captures", "interp_transport",
+              "sourced", "max_draws_per_history"):
+        assert a.counters[k] == b.counters[k], k
+    parent, ordinal = a.bank.parent, a.bank.ordinal
+    key = parent.astype(np.int64) * 64 + ordinal
+    assert np.all(np.diff(key) > 0)
+    assert abs(a.keff.values[0] - b.keff.values[0]) <= 1e-12 * a.keff.values[0]
