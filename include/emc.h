@@ -182,6 +182,24 @@ int emc_upload_union(emc_ctx *ctx, const double *ugrid, int64_t n, const int32_t
  * log-hash + scan, bit-identical to the binary search), 1 double_index,
  * 2 unionized (kernels.py ACCEL_* codes; K:306-320) */
 int emc_set_accel(emc_ctx *ctx, int32_t accel);
+/* Single-process multi-GPU group (SURVEY 8b's init-over-devices, bank
+ * exchange and bin all-reduce entries; replication.py:155-286 with W
+ * workers): ranks = contexts configured for the contiguous particle blocks
+ * [r*P/W, (r+1)*P/W), one per GPU (a GPU may hold several, e.g. for tests).
+ * After every rank's emc_run_batch:
+ *   emc_group_reduce_bins(g, out, n_bins): tallies over the ranks --
+ *     deterministic: chained fold, bit-identical to one rank; fast: rank-ordered
+ *     sum of the rank bins (R:238-240);
+ *   emc_group_exchange_bank(g, ppb, u, &n): every rank's resampling window of
+ *     the global canonical bank (rank-ordered concatenation, R:221-228) copied
+ *     device to device (peer copies) and installed as its source (replaces
+ *     emc_set_source_local, R:271-280); n = global bank size. */
+typedef struct emc_group emc_group;
+int emc_group_create(emc_ctx *const *ctxs, int32_t n, emc_group **out);
+void emc_group_destroy(emc_group *g);
+int emc_group_reduce_bins(emc_group *g, double *out, int64_t n_bins);
+int emc_group_exchange_bank(emc_group *g, int64_t ppb, double u, int64_t *out_n);
+
 /* kernels.macro_lookup_full (kernels.py:287-331): sums[n][5], partials[n][max_comp][4] (nullable) */
 int emc_xs_lookup(emc_ctx *ctx, int64_t n, const int32_t *mats, const double *E, double *sums,
                   double *partials, int32_t max_comp);

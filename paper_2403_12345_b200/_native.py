@@ -84,6 +84,10 @@ SYMBOLS = {
     "emc_grid_index": (C.c_int, [_P, _I64, _P, _P, _P]),
     "emc_upload_union": (C.c_int, [_P, _P, _I64, _P, _P]),
     "emc_set_accel": (C.c_int, [_P, _I32]),
+    "emc_group_create": (C.c_int, [_P, _I32, _P]),
+    "emc_group_destroy": (None, [_P]),
+    "emc_group_reduce_bins": (C.c_int, [_P, _P, _I64]),
+    "emc_group_exchange_bank": (C.c_int, [_P, _I64, _D, _P]),
     "emc_locate": (C.c_int, [_P, _I64, _P, _P]),
     "emc_distance": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P]),
     "emc_particle_ops": (C.c_int, [_P, _I64, _P, _P, _P, _P, _P, _P]),

@@ -1579,3 +1579,5 @@ extern "C" int emc_bench_lookup(emc_ctx* c, int64_t n, const int32_t* mats, cons
     dm.release(); de.release(); dout.release(); dk.release();
     return 0;
 }
+
+#include "emc_group.cuh"

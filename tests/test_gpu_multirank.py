@@ -146,3 +146,74 @@ def test_thread_ranks_fast_reduction_and_errors(golden):
         P.run_replicated(P.RunConfig(particles_per_batch=2, inactive_batches=1, active_batches=0,
                                      mode="event", seed=1, workers=2),
                          scatter, P.analytic_infinite_medium()[1], devices=[0, 0])
+
+
+def _group_run(run, pm, lib, world):
+    """A minimal host coordinator over the C-ABI group entry points (what a
+    non-Python host would write): W contexts, one particle block each, then per
+    batch emc_run_batch on every rank, emc_group_reduce_bins, k, and
+    emc_group_exchange_bank for the next batch's source."""
+    import ctypes as C
+    import hashlib
+
+    import paper_2403_12345_b200 as P
+    from paper_2403_12345_b200 import _native as N
+    from paper_2403_12345_b200 import prng
+    from paper_2403_12345_b200.distributed import block_of
+    from paper_2403_12345_b200.engine import DeviceEngine
+    from paper_2403_12345_b200.tally import TallyLayout
+    cell = P.Pincell(n_axial=pm["n_axial"], fuel_material_ids=pm["fuel_material_ids"],
+                     moderator_material_id=pm["moderator_material_id"])
+    cfg = P.RunConfig(**dict(run["config"], workers=world))
+    ppb = cfg.particles_per_batch
+    engs = []
+    for r in range(world):
+        e = DeviceEngine(0)
+        e.upload_library(lib)
+        e.upload_geometry(cell)
+        e.set_extensions(cell, cfg)
+        lo, hi = block_of(r, world, ppb)
+        e.configure(cfg, lo, hi - lo)
+        engs.append(e)
+    lay = TallyLayout(cell.n_axial)
+    arr = (C.c_void_p * world)(*[e._h.value for e in engs])
+    grp = C.c_void_p()
+    N.check(engs[0].lib.emc_group_create(arr, world, C.byref(grp)), "emc_group_create")
+    try:
+        keff, sums_all, k_run = [], [], 1.0
+        for b in range(cfg.n_batches):
+            for e in engs:
+                out = e.run_batch(b, k_run, batch0=(b == 0), score=b >= cfg.inactive_batches)
+                assert out.error == 0
+            sums = np.zeros(lay.n_bins)
+            N.check(engs[0].lib.emc_group_reduce_bins(grp, N.ptr(sums), lay.n_bins), "emc_group_reduce_bins")
+            sums_all.append(sums)
+            keff.append(sums[lay.keff_bin] / ppb)
+            if b < cfg.n_batches - 1:
+                u, _ = prng.next_uniform(prng.batch_stream(cfg.seed, b))
+                n = C.c_int64()
+                N.check(engs[0].lib.emc_group_exchange_bank(grp, ppb, u, C.byref(n)), "emc_group_exchange_bank")
+                k_run = keff[-1]
+        cols = [np.concatenate(c) for c in zip(*[e.bank_to_host() for e in engs])]
+        bank = P.FissionBank(*cols)
+        h = hashlib.sha256()
+        h.update(np.ascontiguousarray(np.array(keff)).tobytes())
+        h.update(np.ascontiguousarray(np.array(sums_all)).tobytes())
+        h.update(bank.tobytes())
+        return h.hexdigest(), np.array(keff)
+    finally:
+        engs[0].lib.emc_group_destroy(grp)
+        for e in engs:
+            e.close()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_c_abi_group_matches_reference_fingerprint(golden, world):
+    """The C-ABI multi-GPU group (emc_group_*) driven by a minimal coordinator
+    with W contexts on cuda:0 reproduces the reference's C1 fingerprint."""
+    run = golden["runs"]["c1_event"]
+    pm = golden["problems"]["c1"]
+    fp, keff = _group_run(run, pm, golden_library(run["problem"]), world)
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "run_c1_event.npz"))
+    assert np.array_equal(keff, z["keff"])
+    assert fp == run["fingerprint"]
