@@ -158,6 +158,8 @@ def lookup_counters(args, ppb: int) -> dict:
             prof = json.load(fh)
     except (OSError, ValueError):
         return {"source": None, "error": err}
+    if prof.get("workload", "c4") != args.workload:
+        return {"source": None, "error": err or f"committed counters are for {prof.get('workload', 'c4')}"}
     prof["source"] = f"profiles/{LOOKUP_COUNTERS} ({prof.get('command', 'ncu')})"
     prof["current"] = prof.get("csrc_hash") == csrc_hash()
     if err:
@@ -438,7 +440,8 @@ def run_ours(args):
     # roofline: the lookup's binding unit is the L1TEX data pipe (shared-memory
     # staged records), not HBM -- wavefronts per nuclide-lookup from ncu on this
     # build x this run's nuclide-lookups / this run's lookup time (CUDA events)
-    prof = lookup_counters(args, ppb_gpu) if ws == 1 and not c5 else {"source": None}
+    # (gather-lookup workloads -- C1, C5 -- have no staged lookup to sample)
+    prof = lookup_counters(args, ppb_gpu) if ws == 1 and args.workload not in ("c1", "c5") else {"source": None}
     wf = prof.get("l1_wavefronts_per_nuclide_lookup")
     l1_peak = l1_ach = None
     if wf and prof.get("l1_wavefront_peak_per_cycle") and lk_time:
@@ -492,6 +495,14 @@ def run_ours(args):
         "box_guard_events": res.counters.get("box_guard"),
         "timings_s": {k: v for k, v in res.timings.items() if isinstance(v, float)},
     }
+    if l1_ach is None:
+        # no staged-lookup counters (gather-lookup workloads, or ncu unavailable):
+        # the HBM gather model of SURVEY 8d is the roofline reported
+        r = line["roofline"]
+        r.update(bound="hbm", achieved=achieved, peak=peak, unit="GB/s",
+                 frac=(achieved / peak) if achieved else None, traffic=None,
+                 meaning="north_star's HBM gather model: 64 B per nuclide-lookup / summed lookup time vs the "
+                         "measured HBM peak (no L1TEX counters for this workload)")
     if ws == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         line["cpu_baseline"] = cpu_baseline(args, lib, cell, threads, args.cpu_particles or (

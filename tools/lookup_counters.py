@@ -148,6 +148,7 @@ def capture(particles: int, workload: str, sample=None, timeout: int = 900, log:
     what = (f"k_lookup_piped launches {sample[0]}..{sample[0] + len(launches) - 1}" if sample else
             "every lookup launch") + f" of one {workload} batch ({particles} particles), profile_step.py"
     res = summarise(launches, nl, "ncu --metrics ... " + what)
+    res["workload"] = workload
     res["capture_wall_s"] = time.time() - t0
     return res
 
