@@ -519,11 +519,21 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                                 sf[p] = __dadd_rn(sf[p], __dmul_rn(dd.x, ff[p]));
                                 snf[p] = __dadd_rn(snf[p], __dmul_rn(dd.y, ff[p]));
                             }
+                            if constexpr (kCkptStride < LK_G) {   // checkpoints inside the stage
+                                if (ckon && (j + 1) % kCkptStride == 0 && k + 1 <= ncomp) {
+                                    const int32_t row = (k + 1) / kCkptStride - 1;
+#pragma unroll
+                                    for (int p = 0; p < PPL; ++p) {
+                                        double* ckb = MODE == 0 ? ckpt_of(S, s[p]) : bout + n + i[p];
+                                        if (mine[p] && row < nck) ckb[(int64_t)row * cks] = st[p];
+                                    }
+                                }
+                            }
                         }
                         // prefix checkpoint after every kCkptStride nuclides (whole stages)
-                        static_assert(kCkptStride % LK_G == 0, "checkpoints at stage boundaries");
-                        constexpr int CKS = kCkptStride / LK_G;
-                        if (ckon && (t + 1) % CKS == 0 && (t + 1) * LK_G <= ncomp) {
+                        static_assert(kCkptStride % LK_G == 0 || LK_G % kCkptStride == 0, "checkpoint stride");
+                        constexpr int CKS = kCkptStride >= LK_G ? kCkptStride / LK_G : 1;
+                        if (kCkptStride >= LK_G && ckon && (t + 1) % CKS == 0 && (t + 1) * LK_G <= ncomp) {
                             const int32_t row = (t + 1) / CKS - 1;
 #pragma unroll
                             for (int p = 0; p < PPL; ++p) {
@@ -795,6 +805,13 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                         sc = __dadd_rn(sc, __dmul_rn(dd.x, cc));
                         sf = __dadd_rn(sf, __dmul_rn(dd.x, ff));
                         snf = __dadd_rn(snf, __dmul_rn(dd.y, ff));
+                        if constexpr (kCkptStride < LK_G) {       // checkpoints inside the stage
+                            if (ckon && (j + 1) % kCkptStride == 0 && k + 1 <= ncomp) {
+                                const int32_t row = (k + 1) / kCkptStride - 1;
+                                double* ckb = MODE == 0 ? ckpt_of(S, s) : bout + n + i;
+                                if (mine && row < nck) ckb[(int64_t)row * cks] = st;
+                            }
+                        }
                     }
                 } else if (any) {
 #pragma unroll
@@ -823,11 +840,18 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                         sc = __dadd_rn(sc, __dmul_rn(dd.x, cc));
                         sf = __dadd_rn(sf, __dmul_rn(dd.x, ff));
                         snf = __dadd_rn(snf, __dmul_rn(dd.y, ff));
+                        if constexpr (kCkptStride < LK_G) {       // checkpoints inside the stage
+                            if (ckon && (j + 1) % kCkptStride == 0 && k + 1 <= ncomp) {
+                                const int32_t row = (k + 1) / kCkptStride - 1;
+                                double* ckb = MODE == 0 ? ckpt_of(S, s) : bout + n + i;
+                                if (mine && row < nck) ckb[(int64_t)row * cks] = st;
+                            }
+                        }
                     }
                 }
                 if (any) {
-                    constexpr int CKS = kCkptStride / LK_G;
-                    if (ckon && (t + 1) % CKS == 0 && (t + 1) * LK_G <= ncomp) {
+                    constexpr int CKS = kCkptStride >= LK_G ? kCkptStride / LK_G : 1;
+                    if (kCkptStride >= LK_G && ckon && (t + 1) % CKS == 0 && (t + 1) * LK_G <= ncomp) {
                         const int32_t row = (t + 1) / CKS - 1;
                         double* ckb = MODE == 0 ? ckpt_of(S, s) : bout + n + i;
                         if (mine && row < nck) ckb[(int64_t)row * cks] = st;
