@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define EMC_ABI_VERSION 1
+#define EMC_ABI_VERSION 2   /* 2: box_guard in emc_run_config; grid index, union backends, groups */
 #define EMC_N_COUNTERS 24   /* kernels.py:81-103 layout */
 #define EMC_N_TIMINGS 4     /* kernels.py:115-120: lookup, advance, collision, sort */
 

@@ -14,6 +14,7 @@ import os
 from .errors import NativeUnavailableError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+ABI_VERSION = 2                     # include/emc.h EMC_ABI_VERSION
 LIB_PATH = os.environ.get("EMC_LIBRARY") or os.path.join(HERE, "libemc.so")
 
 N_COUNTERS = 24
@@ -117,6 +118,9 @@ def load_library_file() -> C.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if lib.emc_abi_version() != ABI_VERSION:
+        raise NativeUnavailableError(f"{LIB_PATH} has ABI {lib.emc_abi_version()}, these bindings need "
+                                     f"{ABI_VERSION}: rebuild it (python -m paper_2403_12345_b200._build)")
     _LIB = lib
     return lib
 

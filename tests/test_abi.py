@@ -27,7 +27,7 @@ def test_library_exports_every_symbol():
     lib = _native.load_library_file()
     for name in _declared():
         assert hasattr(lib, name), name
-    assert lib.emc_abi_version() == 1
+    assert lib.emc_abi_version() == _native.ABI_VERSION == 2
 
 
 def test_no_cpu_fallback():
