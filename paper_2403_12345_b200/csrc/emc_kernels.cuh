@@ -18,7 +18,7 @@ namespace emc {
 // their registers so enough warps are resident to hide the gather latency
 // (measured: collision 80 -> 63 ms per C4 batch at 4 blocks/SM).
 #ifndef EMC_ADV_MINB
-#define EMC_ADV_MINB 3
+#define EMC_ADV_MINB 2
 #endif
 #ifndef EMC_COL_MINB
 #define EMC_COL_MINB 4
@@ -410,18 +410,49 @@ __global__ void __launch_bounds__(256, 4) k_lookup_bench(int32_t n, DLib L, cons
 // (fast reduction): one warp reduction + atomic per distinct region in the
 // warp for up to three regions (energy-major queues mix a few materials per
 // warp), per-lane atomics for the rest.
+//
+// The five sums of a round are a reduce-scatter butterfly rather than five
+// all-reduces: at xor 16 the lower half-warp keeps scores 0-2 and the upper
+// 3-4, at xor 8 the 3-value quarters split {0,2}|{1} and the others {3}|{4},
+// at xor 4 the one 2-value group splits; xor 2 and xor 1 finish.  8 f64
+// shuffles instead of 25, and the five atomics are one instruction issued by
+// lanes 0, 8, 4, 16, 24 (scores 0, 1, 2, 3, 4).
+#ifndef EMC_SCORE_BFLY
+#define EMC_SCORE_BFLY 1
+#endif
 __device__ __forceinline__ void score_bins(double* bins, bool valid, int32_t base, const double v[5])
 {
     unsigned todo = __ballot_sync(kFull, valid);
+    const unsigned ln = lane_id();
     for (int round = 0; round < 3 && todo; ++round) {
         const int l = __ffs(todo) - 1;
         const int32_t b = __shfl_sync(kFull, base, l);
         const bool in = valid && base == b;
         todo &= ~__ballot_sync(kFull, in);
-        #pragma unroll
-        for (int k = 0; k < 5; ++k) {
-            double s = warp_sum_f64(in ? v[k] : 0.0);
-            if ((int)lane_id() == l && s != 0.0) atomicAdd(bins + b + k, s);
+        if (EMC_SCORE_BFLY) {
+            double x0 = in ? v[0] : 0.0, x1 = in ? v[1] : 0.0, x2 = in ? v[2] : 0.0;
+            double x3 = in ? v[3] : 0.0, x4 = in ? v[4] : 0.0;
+            const bool h16 = ln & 16, h8 = ln & 8, h4 = ln & 4;
+            // xor 16: lower keeps (0,1,2), upper keeps (3,4,-)
+            double a0 = (h16 ? x3 : x0) + __shfl_xor_sync(kFull, h16 ? x0 : x3, 16);
+            double a1 = (h16 ? x4 : x1) + __shfl_xor_sync(kFull, h16 ? x1 : x4, 16);
+            double a2 = (h16 ? 0.0 : x2) + __shfl_xor_sync(kFull, h16 ? x2 : 0.0, 16);
+            // xor 8: keep (a0, a2) below, (a1, -) above
+            double b0 = (h8 ? a1 : a0) + __shfl_xor_sync(kFull, h8 ? a0 : a1, 8);
+            double b1 = (h8 ? 0.0 : a2) + __shfl_xor_sync(kFull, h8 ? a2 : 0.0, 8);
+            // xor 4: keep b0 below, b1 above
+            double c0 = (h4 ? b1 : b0) + __shfl_xor_sync(kFull, h4 ? b0 : b1, 4);
+            c0 += __shfl_xor_sync(kFull, c0, 2);
+            c0 += __shfl_xor_sync(kFull, c0, 1);
+            // lane -> score: 0->0, 4->2, 8->1, 16->3, 24->4
+            const int k = ln == 0 ? 0 : ln == 4 ? 2 : ln == 8 ? 1 : ln == 16 ? 3 : ln == 24 ? 4 : -1;
+            if (k >= 0 && c0 != 0.0) atomicAdd(bins + b + k, c0);
+        } else {
+            #pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                double s = warp_sum_f64(in ? v[k] : 0.0);
+                if ((int)ln == l && s != 0.0) atomicAdd(bins + b + k, s);
+            }
         }
         if (in) valid = false;
     }
