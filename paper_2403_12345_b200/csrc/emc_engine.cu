@@ -912,7 +912,7 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
                 continue;
             }
             const int32_t* q = cur;
-            EMC_TRY_CUDA(cudaMemsetAsync(&c->ctl.p->nL2, 0, 3 * sizeof(unsigned), st));
+            EMC_TRY_CUDA(cudaMemsetAsync(&c->ctl.p->nL2, 0, (char*)(&c->ctl.p->nX + 1) - (char*)&c->ctl.p->nL2, st));
             bool do_sort = cf.sort_enabled && nL > 1 && (look_inv % cf.sort_every) == 0;
             EMC_TRY_CUDA(cudaEventRecord(c->ev[0], st));
             if (do_sort) {

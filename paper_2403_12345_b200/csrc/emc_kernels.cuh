@@ -61,6 +61,33 @@ __device__ __forceinline__ void queue_push_key(int32_t* q, unsigned int* count, 
     }
 }
 
+// The advance's three queue pushes (collision, next lookup with its sort key,
+// leakage) with their tail atomics issued by lanes 0, 1, 2 in ONE atomic
+// instruction: the warp waits for one round trip instead of three.
+#ifndef EMC_PUSH3
+#define EMC_PUSH3 1
+#endif
+__device__ __forceinline__ void queue_push3(int32_t slot, int32_t* q0, unsigned int* c0, bool p0,
+                                            int32_t* q1, unsigned int* c1, bool p1, uint32_t* keys, uint32_t key,
+                                            int32_t* q2, unsigned int* c2, bool p2)
+{
+    const unsigned m0 = __ballot_sync(kFull, p0), m1 = __ballot_sync(kFull, p1), m2 = __ballot_sync(kFull, p2);
+    const unsigned ln = lane_id(), below = (1u << ln) - 1u;
+    const unsigned m = ln == 0 ? m0 : ln == 1 ? m1 : m2;
+    unsigned int* cp = ln == 0 ? c0 : ln == 1 ? c1 : c2;
+    unsigned base = 0;
+    if (ln < 3 && m) base = atomicAdd(cp, (unsigned int)__popc(m));
+    const unsigned b0 = __shfl_sync(kFull, base, 0), b1 = __shfl_sync(kFull, base, 1),
+                   b2 = __shfl_sync(kFull, base, 2);
+    if (p0) q0[b0 + __popc(m0 & below)] = slot;
+    if (p1) {
+        const unsigned at = b1 + __popc(m1 & below);
+        q1[at] = slot;
+        if (keys) keys[at] = key;
+    }
+    if (p2) q2[b2 + __popc(m2 & below)] = slot;
+}
+
 // Lookup-queue sort keys written at push time (energy-major key of
 // k_sort_keys<true>): the kernels that put a particle on the next lookup
 // queue know its energy and material, so the sort needs no separate gather
@@ -652,11 +679,17 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
         }
         if (moved) { PState& p = S.ps[s]; p.a = a; p.b = b; }
         if (to_col || to_cross) S.ps[s].d = d;
-        queue_push(q_col, &ctl->nC, s, to_col);
         const bool to_next = to_cross && !leak;
-        queue_push_key(q_next, &ctl->nL2, s, to_next, K.keys,
-                       (to_next && K.keys) ? lookup_key(L, K, kE, d.mat) : 0u);
-        if (G.vacuum) queue_push(q_cross, &ctl->nX, s, to_cross && leak);
+        if (EMC_PUSH3) {
+            queue_push3(s, q_col, &ctl->nC, to_col, q_next, &ctl->nL2, to_next, K.keys,
+                        (to_next && K.keys) ? lookup_key(L, K, kE, d.mat) : 0u,
+                        q_cross, &ctl->nX, G.vacuum && to_cross && leak);
+        } else {
+            queue_push(q_col, &ctl->nC, s, to_col);
+            queue_push_key(q_next, &ctl->nL2, s, to_next, K.keys,
+                           (to_next && K.keys) ? lookup_key(L, K, kE, d.mat) : 0u);
+            if (G.vacuum) queue_push(q_cross, &ctl->nX, s, to_cross && leak);
+        }
     }
     warp_add_u64(cnt + CNT_INTERP_SCORE, interp_score);
     warp_add_u64(cnt + CNT_EV_LOOKUP, chained);
@@ -844,6 +877,29 @@ __device__ __forceinline__ int32_t select_nuclide(const DLib& L, const double* c
     return ksel;
 }
 
+// two warp claims in one atomic round trip: n0 entries per lane from cur0
+// (lane 31 issues), one entry per lane with p1 from cur1 (lane 30 issues)
+#ifndef EMC_CLAIM2
+#define EMC_CLAIM2 1
+#endif
+__device__ __forceinline__ void warp_claim2(unsigned long long* cur0, unsigned int n0, unsigned long long& at0,
+                                            unsigned long long* cur1, bool p1, unsigned long long& at1)
+{
+    unsigned int incl = n0;
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned int y = __shfl_up_sync(kFull, incl, o);
+        if ((int)lane_id() >= o) incl += y;
+    }
+    const unsigned int total = __shfl_sync(kFull, incl, 31);
+    const unsigned m1 = __ballot_sync(kFull, p1);
+    const unsigned ln = lane_id();
+    const unsigned int add = ln == 31 ? total : __popc(m1);
+    unsigned long long base = 0;
+    if (ln >= 30 && add) base = atomicAdd(ln == 31 ? cur0 : cur1, (unsigned long long)add);
+    at0 = __shfl_sync(kFull, base, 31) + (incl - n0);
+    at1 = __shfl_sync(kFull, base, 30) + (unsigned long long)__popc(m1 & ((1u << ln) - 1u));
+}
+
 // K:814-923 + refill (K:1187-1202)
 __global__ void __launch_bounds__(256, EMC_COL_MINB) k_collision(const int32_t* __restrict__ q, const unsigned int* nq,
                                                    BatchP bp, DLib L, DGeom G, DSrc src, DSlots S,
@@ -916,8 +972,17 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_collision(const int32_t* 
         } else {
             warp_add_f64(bins + bp.kbin, valid ? kval : 0.0);
         }
-        // fission sites (K:913-922); the site draws continue the parent stream
-        unsigned long long at = warp_claim(&ctl->site_n, nsites);
+        // fission sites (K:913-922); the site draws continue the parent stream.
+        // Each site takes 3 draws, so the stream-overlap check (K:1183-1186)
+        // is known here, and the site claim and the batch-cursor claim for
+        // the dead slots go out as one atomic instruction (EMC_CLAIM2).
+        const bool overlap = valid && (alive || died) && d.draws + 3 * (int32_t)nsites >= kStride;
+        unsigned long long at, idx = 0;
+        if (EMC_CLAIM2) {
+            warp_claim2(&ctl->site_n, nsites, at, &ctl->cursor, died && !overlap, idx);
+        } else {
+            at = warp_claim(&ctl->site_n, nsites);
+        }
         for (unsigned ms = 0; ms < nsites; ++ms) {
             double ua = draw(b.rng, d.draws), ub = draw(b.rng, d.draws);
             double sx, sy, sz;
@@ -930,7 +995,7 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_collision(const int32_t* 
             sb.x[w] = a.x; sb.y[w] = a.y; sb.z[w] = a.z;
             sb.dx[w] = sx; sb.dy[w] = sy; sb.dz[w] = sz; sb.E[w] = es;
         }
-        if (valid && (alive || died) && d.draws >= kStride) {      // K:1183-1186
+        if (overlap) {                                           // K:1183-1186
             set_error(ctl, cnt, ERR_STREAM_OVERLAP, d.gid);
             alive = died = false;
         }
@@ -944,7 +1009,7 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_collision(const int32_t* 
             maxhist = max(maxhist, (unsigned long long)d.histlog);
         }
         // claim the next source particle for dead slots
-        unsigned long long idx = warp_claim(&ctl->cursor, died ? 1u : 0u);
+        if (!EMC_CLAIM2) idx = warp_claim(&ctl->cursor, died ? 1u : 0u);
         if (died && idx < (unsigned long long)bp.n_assigned) {
             refill = source_particle(s, bp.g_lo + (int64_t)idx, bp, L, G, src, S, ctl, clamps);
             sourced += 1;
