@@ -879,6 +879,9 @@ __device__ __forceinline__ int32_t select_nuclide(const DLib& L, const double* c
 
 // two warp claims in one atomic round trip: n0 entries per lane from cur0
 // (lane 31 issues), one entry per lane with p1 from cur1 (lane 30 issues)
+#ifndef EMC_COL_PREFETCH
+#define EMC_COL_PREFETCH 0   // measured: collision +2% slower with it
+#endif
 #ifndef EMC_CLAIM2
 #define EMC_CLAIM2 1
 #endif
@@ -914,6 +917,7 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_collision(const int32_t* 
         int64_t i = emc_base_ + lane_id();
         bool valid = i < n;
         int32_t s = valid ? q[i] : 0;
+        if (EMC_COL_PREFETCH) prefetch_next_line(q, i, emc_stride_, n, S.ps);
         bool alive = false, died = false;
         double kval = 0.0;
         unsigned nsites = 0;
