@@ -222,6 +222,11 @@ extern "C" int emc_create(int device, emc_ctx** out)
     emc_ctx* c = new emc_ctx();
     c->device = device;
     cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+    {
+        uint64_t tab[2][64];
+        lcg_gskip_table(tab);
+        EMC_TRY_CUDA(cudaMemcpyToSymbol(c_gskip, tab, sizeof(tab)));
+    }
     if (cudaMallocHost(&c->ctl_host, sizeof(Ctl)) != cudaSuccess) { delete c; g_err = "cudaMallocHost"; return EMC_E_CUDA; }
     if (c->ctl.alloc(1) || c->cnt.alloc(EMC_N_COUNTERS)) { delete c; return EMC_E_OOM; }
     for (auto& e : c->ev) cudaEventCreate(&e);
@@ -758,6 +763,7 @@ static int run_batch_once(emc_ctx* c, const emc_batch_args* a, emc_batch_result*
     bp.fused = cf.fused; bp.score = a->score; bp.use_logs = cf.use_logs; bp.batch0 = a->batch0;
     bp.kbin = c->kbin; bp.history = cf.history;
     bp.fixed_source = c->fixed_source; bp.src_energy = c->src_energy;
+    bp.seed_b = lcg_skip(bp.seed, (uint64_t)bp.batch * (uint64_t)bp.pmax * (uint64_t)kStride);
     if (!a->batch0 && !c->fixed_source && (c->src.n < 1 || !c->src.x))
         return fail_arg("batch > 0 needs a source bank (emc_set_source_*)");
 

@@ -129,8 +129,13 @@ __device__ __forceinline__ bool source_particle(int32_t slot, int64_t g, const B
                                                 const DLib& L, const DGeom& G, const DSrc& src,
                                                 const DSlots& S, Ctl* ctl, int& clamps)
 {
-    uint64_t off = ((uint64_t)bp.batch * (uint64_t)bp.pmax + (uint64_t)g) * (uint64_t)kStride;
-    uint64_t s = lcg_skip(bp.seed, off);
+    uint64_t s;
+    if (EMC_GSKIP) {
+        s = lcg_gskip(bp.seed_b, (uint64_t)g);
+    } else {
+        uint64_t off = ((uint64_t)bp.batch * (uint64_t)bp.pmax + (uint64_t)g) * (uint64_t)kStride;
+        s = lcg_skip(bp.seed, off);
+    }
     if (g == bp.perturb_gid) s ^= 1ULL;
     int32_t draws = 0;
     P0 a; P1 b;
