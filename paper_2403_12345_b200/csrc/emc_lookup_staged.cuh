@@ -770,6 +770,11 @@ __global__ void __launch_bounds__(NW * 32, MINB)
             const int32_t mu = mine ? m : ms;
             double st = 0.0, sc = 0.0, sf = 0.0, snf = 0.0;
             const long long Eb = __double_as_longlong(Eu);
+            // checkpoint rows this lane stores in this pass: row r (after
+            // nuclide (r+1)*stride) exists iff (r+1)*stride <= ncomp and r < nck;
+            // one compare per checkpoint instead of (ckon, mine, ncomp, nck)
+            const int32_t ck_rows = (ckon && mine) ? min(nck, ncomp / kCkptStride) : 0;
+            double* const ckp = MODE == 0 ? ckpt_of(S, s) : bout + n + i;
             for (int t = 0; t < nst; ++t, ++T) {
                 const int d = (int)(T % LK_D);
                 mbar_wait(&sh.full[d], (T / LK_D) & 1, 0x20000u | T);
@@ -806,10 +811,9 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                         sf = __dadd_rn(sf, __dmul_rn(dd.x, ff));
                         snf = __dadd_rn(snf, __dmul_rn(dd.y, ff));
                         if constexpr (kCkptStride < LK_G) {       // checkpoints inside the stage
-                            if (ckon && (j + 1) % kCkptStride == 0 && k + 1 <= ncomp) {
+                            if ((j + 1) % kCkptStride == 0) {
                                 const int32_t row = (k + 1) / kCkptStride - 1;
-                                double* ckb = MODE == 0 ? ckpt_of(S, s) : bout + n + i;
-                                if (mine && row < nck) ckb[(int64_t)row * cks] = st;
+                                if (row < ck_rows) ckp[(int64_t)row * cks] = st;
                             }
                         }
                     }
@@ -841,20 +845,18 @@ __global__ void __launch_bounds__(NW * 32, MINB)
                         sf = __dadd_rn(sf, __dmul_rn(dd.x, ff));
                         snf = __dadd_rn(snf, __dmul_rn(dd.y, ff));
                         if constexpr (kCkptStride < LK_G) {       // checkpoints inside the stage
-                            if (ckon && (j + 1) % kCkptStride == 0 && k + 1 <= ncomp) {
+                            if ((j + 1) % kCkptStride == 0) {
                                 const int32_t row = (k + 1) / kCkptStride - 1;
-                                double* ckb = MODE == 0 ? ckpt_of(S, s) : bout + n + i;
-                                if (mine && row < nck) ckb[(int64_t)row * cks] = st;
+                                if (row < ck_rows) ckp[(int64_t)row * cks] = st;
                             }
                         }
                     }
                 }
                 if (any) {
                     constexpr int CKS = kCkptStride >= LK_G ? kCkptStride / LK_G : 1;
-                    if (kCkptStride >= LK_G && ckon && (t + 1) % CKS == 0 && (t + 1) * LK_G <= ncomp) {
+                    if (kCkptStride >= LK_G && (t + 1) % CKS == 0) {
                         const int32_t row = (t + 1) / CKS - 1;
-                        double* ckb = MODE == 0 ? ckpt_of(S, s) : bout + n + i;
-                        if (mine && row < nck) ckb[(int64_t)row * cks] = st;
+                        if (row < ck_rows) ckp[(int64_t)row * cks] = st;
                     }
                 }
                 __syncwarp();
