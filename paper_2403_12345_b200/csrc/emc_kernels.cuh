@@ -760,17 +760,26 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_crossing(const int32_t* _
 // last sigma_t prefix checkpoint <= target written by the lookup, so at most
 // kCkptStride partials are re-interpolated (bit-identical to the stored
 // part_t walk).  Naive: re-interpolate from the first nuclide (K:853-883).
-// EMC_CK_ARY > 1: K-ary checkpoint search (K independent probes per round
-// trip).  Measured on C4/C3: binary 0.329 s collision per batch, 4-ary
-// 0.351, 8-ary 0.362, 16-ary 0.363 -- the extra probe sectors cost more HBM
-// traffic than the shorter dependent chain saves, so binary stays.
-#ifndef EMC_CK_ARY
-#define EMC_CK_ARY 1
+// Optional first probe round of the checkpoint search: EMC_CK_WIN independent
+// probes around the row the draw points at, g = floor(u * cmax) (tgt = u *
+// sigma_t and the prefix grows about linearly in the checkpoint index for
+// the benchmark libraries: the answer is in [g-1, g+3] for ~99% of
+// collisions, measured offline on the C4 library), then the binary search on
+// what is left.  The result is the same row whatever the probes (the
+// predicate is monotone).  Measured SLOWER (C4 collision +10% at 6 probes,
+// +9% at 4, +14% at 8): the queue is in slot order and every lane of a warp
+// with the same material starts the binary search on the same row, so its
+// first levels are coalesced loads (2 lines per warp) -- only its last ~3
+// levels scatter, while every window probe is per-lane (a sector per lane).
+// An evenly spaced K-ary round (same rows for the whole warp) then leaves K
+// scattered probes instead of ~3: also slower.  Default 0: binary search.
+#ifndef EMC_CK_WIN
+#define EMC_CK_WIN 0
 #endif
-constexpr int kCkAry = EMC_CK_ARY;
+constexpr int kCkWin = EMC_CK_WIN;
 __device__ __forceinline__ int32_t select_nuclide(const DLib& L, const double* ck, int32_t nck, int64_t cks,
                                                   int32_t e0,
-                                                  int32_t e1, int32_t bin, double E, double tgt,
+                                                  int32_t e1, int32_t bin, double E, double u, double tgt,
                                                   bool fused, double& pt_sel, unsigned long long& interp)
 {
     int32_t ncomp = e1 - e0;
@@ -780,34 +789,22 @@ __device__ __forceinline__ int32_t select_nuclide(const DLib& L, const double* c
         int32_t cmax = (ncomp - 1) / kCkptStride;
         if (cmax > nck) cmax = nck;
         int32_t lo = 0, hi = cmax;      // largest c with P_c <= tgt (P_0 = 0)
-        if (kCkAry <= 1) {
-            while (lo < hi) {
-                int32_t mid = (lo + hi + 1) >> 1;
-                if (ck[(int64_t)(mid - 1) * cks] <= tgt) lo = mid; else hi = mid - 1;
+        if (kCkWin > 0 && cmax > 0) {
+            const int32_t g = (int32_t)__dmul_rn(u, (double)cmax);
+            const int32_t r0 = max(1, min(g - 1, cmax - kCkWin + 1));
+            double pv[kCkWin > 0 ? kCkWin : 1];
+            #pragma unroll
+            for (int j = 0; j < kCkWin; ++j) pv[j] = ck[(int64_t)(min(r0 + j, cmax) - 1) * cks];
+            #pragma unroll
+            for (int j = 0; j < kCkWin; ++j) {
+                const int32_t r = min(r0 + j, cmax);
+                if (pv[j] <= tgt) lo = max(lo, r);
+                else hi = min(hi, r - 1);
             }
-        } else {
-            // kCkAry-ary search: kCkAry independent probes per round trip
-            // (the checkpoints live in HBM, one sector per probe, so the
-            // dependent-load chain, not the bytes, is what a binary search
-            // costs); probes m_j = lo + ((j+1) span + K) / (K+1) lie in
-            // [lo+1, hi] and cover it once span <= K+1
-            while (lo < hi) {
-                const int32_t span = hi - lo;
-                double pv[kCkAry];
-                int32_t mv[kCkAry];
-                #pragma unroll
-                for (int j = 0; j < kCkAry; ++j) {
-                    mv[j] = lo + ((j + 1) * span + kCkAry) / (kCkAry + 1);
-                    pv[j] = ck[(int64_t)(mv[j] - 1) * cks];
-                }
-                int32_t nlo = lo, nhi = hi;
-                #pragma unroll
-                for (int j = 0; j < kCkAry; ++j) {
-                    if (pv[j] <= tgt) nlo = max(nlo, mv[j]);
-                    else nhi = min(nhi, mv[j] - 1);
-                }
-                lo = nlo; hi = nhi;
-            }
+        }
+        while (lo < hi) {
+            int32_t mid = (lo + hi + 1) >> 1;
+            if (ck[(int64_t)(mid - 1) * cks] <= tgt) lo = mid; else hi = mid - 1;
         }
         c = lo;
         if (c > 0) cum = ck[(int64_t)(c - 1) * cks];
@@ -939,7 +936,7 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_collision(const int32_t* 
             double u1 = draw(b.rng, d.draws);
             double tgt = __dmul_rn(u1, st);
             double pt_sel;
-            int32_t ksel = select_nuclide(L, ckpt_of(S, s), S.nck, S.ck_row, e0, e1, bin, E, tgt,
+            int32_t ksel = select_nuclide(L, ckpt_of(S, s), S.nck, S.ck_row, e0, e1, bin, E, u1, tgt,
                                           bp.fused != 0, pt_sel, interp);
             const Comp cs = L.comp[ksel];
             double s_s, s_c, s_f;
