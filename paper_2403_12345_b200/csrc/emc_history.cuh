@@ -201,7 +201,7 @@ __device__ __forceinline__ bool transport_to_death(int32_t s, int64_t g, uint64_
             double tgt = __dmul_rn(u1, st);
             double pt_sel;
             int32_t ksel = select_nuclide(L, ck, S.nck, S.ck_row, e0, e1, bin, E, u1, tgt, bp.fused != 0, pt_sel, A.interp);
-            const Comp cs = L.comp[ksel];
+            const Comp cs = load_comp(L.comp + ksel);
             double s_s, s_c, s_f;
             micro_scf(L, cs, bin, E, s_s, s_c, s_f);
             A.interp += 3;

@@ -825,7 +825,7 @@ __device__ __forceinline__ int32_t select_nuclide(const DLib& L, const double* c
     int32_t ng0[SN], nlast[SN], nh[SN];
     #pragma unroll
     for (int u = 0; u < SN; ++u) {
-        const Comp cc = L.comp[min(kstart + u, e1 - 1)];
+        const Comp cc = load_comp(L.comp + min(kstart + u, e1 - 1));
         nden[u] = cc.den; ng0[u] = cc.g0; nlast[u] = cc.glen - 1;
         nh[u] = nlast[u] > 0 ? __ldg(L.hash + (int64_t)cc.nid * L.nbins + bin) : 0;
     }
@@ -844,7 +844,7 @@ __device__ __forceinline__ int32_t select_nuclide(const DLib& L, const double* c
         if (k0 + SN < e1) {                       // next group's entries and hash bounds
             #pragma unroll
             for (int u = 0; u < SN; ++u) {
-                const Comp cc = L.comp[min(k0 + SN + u, e1 - 1)];
+                const Comp cc = load_comp(L.comp + min(k0 + SN + u, e1 - 1));
                 nden[u] = cc.den; ng0[u] = cc.g0; nlast[u] = cc.glen - 1;
                 nh[u] = nlast[u] > 0 ? __ldg(L.hash + (int64_t)cc.nid * L.nbins + bin) : 0;
             }
@@ -938,7 +938,7 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_collision(const int32_t* 
             double pt_sel;
             int32_t ksel = select_nuclide(L, ckpt_of(S, s), S.nck, S.ck_row, e0, e1, bin, E, u1, tgt,
                                           bp.fused != 0, pt_sel, interp);
-            const Comp cs = L.comp[ksel];
+            const Comp cs = load_comp(L.comp + ksel);
             double s_s, s_c, s_f;
             micro_scf(L, cs, bin, E, s_s, s_c, s_f);
             interp += 3;

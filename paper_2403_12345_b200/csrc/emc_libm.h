@@ -35,7 +35,14 @@
 
 #if defined(__CUDACC__)
 #define EMC_LIBM_FN __device__ __forceinline__
-#define EMC_TABLE_QUAL __device__ const
+#define EMC_TABLE_QUAL __device__ const __align__(32)
+/* table entries read together in one load (tables 32-byte aligned; on the
+   device a lane's 2 / 4 entries are one 128- / 256-bit request instead of
+   2 / 4 scattered 64-bit ones) */
+#define EMC_TAB2(t, i, a, b) do { const double2 v_ = *reinterpret_cast<const double2*>(&(t)[i]); \
+                                  (a) = v_.x; (b) = v_.y; } while (0)
+#define EMC_TAB4(t, i, a, b, c, d) \
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(&(t)[i]))
 #define EMC_FMA(a, b, c) __fma_rn((a), (b), (c))
 #define EMC_MUL(a, b) __dmul_rn((a), (b))
 #define EMC_ADD(a, b) __dadd_rn((a), (b))
@@ -48,6 +55,8 @@
 #include <string.h>
 #define EMC_LIBM_FN static inline
 #define EMC_TABLE_QUAL const
+#define EMC_TAB2(t, i, a, b) do { (a) = (t)[i]; (b) = (t)[(i) + 1]; } while (0)
+#define EMC_TAB4(t, i, a, b, c, d) do { (a) = (t)[i]; (b) = (t)[(i) + 1]; (c) = (t)[(i) + 2]; (d) = (t)[(i) + 3]; } while (0)
 #define EMC_FMA(a, b, c) fma((a), (b), (c))
 #define EMC_MUL(a, b) ((a) * (b))
 #define EMC_ADD(a, b) ((a) + (b))
@@ -109,8 +118,8 @@ EMC_LIBM_FN double emc_log(double x)
     int i = (int)((tmp >> 45) & 0x7f);
     int32_t k = (int32_t)((int64_t)tmp >> 52);
     uint64_t iz = ix - (tmp & 0xfff0000000000000ULL);
-    double invc = emc_log_tab[2 * i];
-    double logc = emc_log_tab[2 * i + 1];
+    double invc, logc;
+    EMC_TAB2(emc_log_tab, 2 * i, invc, logc);
     double kd = (double)k;
     double z = EMC_AS_F64(iz);
     double w = EMC_FMA(kd, EMC_LOG_LN2HI, logc);
@@ -160,8 +169,8 @@ EMC_LIBM_FN double emc_do_sin_tab_(double x, double dx)
     double u = EMC_ADD(ax, EMC_SC_BIG);
     int k = (int)(uint32_t)EMC_AS_U64(u) << 2;
     double xr = EMC_SUB(ax, EMC_SUB(u, EMC_SC_BIG));
-    double sn = emc_sincostab[k], ssn = emc_sincostab[k + 1];
-    double cs = emc_sincostab[k + 2], ccs = emc_sincostab[k + 3];
+    double sn, ssn, cs, ccs;
+    EMC_TAB4(emc_sincostab, k, sn, ssn, cs, ccs);
     double xx = EMC_MUL(xr, xr);
     double ps = EMC_FMA(xx, EMC_SC_SN5, EMC_SC_SN3);
     double s = EMC_FMA(EMC_MUL(xr, xx), ps, dx);
@@ -188,8 +197,8 @@ EMC_LIBM_FN double emc_do_cos_(double x, double dx)
     double u = EMC_ADD(ax, EMC_SC_BIG);
     int k = (int)(uint32_t)EMC_AS_U64(u) << 2;
     double xr = EMC_ADD(EMC_SUB(ax, EMC_SUB(u, EMC_SC_BIG)), dx);
-    double sn = emc_sincostab[k], ssn = emc_sincostab[k + 1];
-    double cs = emc_sincostab[k + 2], ccs = emc_sincostab[k + 3];
+    double sn, ssn, cs, ccs;
+    EMC_TAB4(emc_sincostab, k, sn, ssn, cs, ccs);
     double xx = EMC_MUL(xr, xr);
     double ps = EMC_FMA(xx, EMC_SC_SN5, EMC_SC_SN3);
     double s = EMC_FMA(EMC_MUL(xr, xx), ps, xr);
