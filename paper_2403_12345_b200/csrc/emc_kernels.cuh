@@ -191,7 +191,7 @@ __device__ __forceinline__ bool source_particle(int32_t slot, int64_t g, const B
     d.gid = g; d.draws = draws; d.ordctr = 0; d.histlog = 0; d.axial = ax; d.mat = mat;
     d.surf = -1; d.kind = (int8_t)kd; d.pad = 0;
     PState& p = S.ps[slot];
-    p.a = a; p.b = b; p.d = d;
+    p.a = a; p.b = b; st_p3(&p.d, d);
     if (kd < 0) { set_error(ctl, nullptr, ERR_OUTSIDE_BOX, g); return false; }
     return true;
 }
@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
         P0 a{}; P1 b{}; P2 c{}; P3 d{};
         if (valid) {
             const PState& p = S.ps[s];
-            a = p.a; b = p.b; c = p.c; d = p.d;
+            a = p.a; b = p.b; c = p.c; d = ld_p3(&p.d);
             if (!(c.t > 0.0)) {
                 set_error(ctl, cnt, ERR_NONPOSITIVE_SIGMA, d.gid);
                 valid = false;
@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
             seg = again;
         }
         if (moved) { PState& p = S.ps[s]; p.a = a; p.b = b; }
-        if (to_col || to_cross) S.ps[s].d = d;
+        if (to_col || to_cross) st_p3(&S.ps[s].d, d);
         const bool to_next = to_cross && !leak;
         if (EMC_PUSH3) {
             queue_push3(s, q_col, &ctl->nC, to_col, q_next, &ctl->nL2, to_next, K.keys,
@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_crossing(const int32_t* _
         int32_t s = valid ? q[i] : 0;
         if (valid) {
             PState& p = S.ps[s];
-            P0 a = p.a; P1 b = p.b; P3 d = p.d;
+            P0 a = p.a; P1 b = p.b; P3 d = ld_p3(&p.d);
             const int32_t surf = d.surf;
             if (surf >= SURF_XMIN && surf <= SURF_ZMAX && G.vacuum) {
                 died = true;
@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_crossing(const int32_t* _
                 maxhist = max(maxhist, (unsigned long long)d.histlog);
             } else {                     // (k_advance completes non-leaking crossings itself)
                 cross_surface(a, b, d, G);
-                p.a = a; p.b = b; p.d = d;
+                p.a = a; p.b = b; st_p3(&p.d, d);
             }
         }
         bool refill = false;
@@ -926,7 +926,7 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_collision(const int32_t* 
         P0 a{}; P1 b{}; P3 d{};
         if (valid) {
             PState& p = S.ps[s];
-            a = p.a; b = p.b; d = p.d;
+            a = p.a; b = p.b; d = ld_p3(&p.d);
             const P2 c = p.c;
             const double st = c.t;
             kval = __dmul_rn(1.0, __ddiv_rn(c.nsf, st));            // wt * (nsf / st)
@@ -1007,7 +1007,7 @@ __global__ void __launch_bounds__(256, EMC_COL_MINB) k_collision(const int32_t* 
         }
         if (alive) {
             PState& p = S.ps[s];
-            p.a = a; p.b = b; p.d = d;
+            p.a = a; p.b = b; st_p3(&p.d, d);
         }
         bool refill = false;
         if (died) {                                              // K:999-1006
