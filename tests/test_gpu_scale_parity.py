@@ -167,6 +167,26 @@ def test_union_backend_run_matches_oracle(accel, c3, c3_index):
     assert res.physics_fingerprint() == want
 
 
+def test_fast_tally_bins_match_deterministic():
+    """The fast reduction's warp-aggregated scoring (reduce-scatter butterfly
+    per region, up to three regions per warp, per-lane atomics beyond) against
+    the deterministic log fold, bin by bin, on the HM core -- 100 axial fuel
+    regions + moderator, so warps mix regions and every scoring branch runs.
+    Batch 0 only (k_run = 1 in both modes: the same histories); atomics only
+    reorder the sums: 1e-11 relative per bin."""
+    lib, cell = P.hm_core(34, 3, 11303, 100, seed=1)
+    res = {}
+    for red in ("fast", "deterministic"):
+        cfg = P.RunConfig(particles_per_batch=300_000, inactive_batches=0, active_batches=1, mode="event",
+                          seed=42, max_in_flight=300_000, reduction=red)
+        res[red] = P.run_replicated(cfg, lib, cell)
+    a, b = np.asarray(res["fast"].batch_sums[0]), np.asarray(res["deterministic"].batch_sums[0])
+    assert a.shape == b.shape and np.count_nonzero(b) > 300
+    assert np.allclose(a, b, rtol=1e-11, atol=0)
+    for k in ("events_lookup", "events_advance", "events_collision", "fissions", "captures"):
+        assert res["fast"].counters[k] == res["deterministic"].counters[k], k
+
+
 @pytest.mark.slow
 def test_deterministic_log_above_int32(engine_env):
     """the deterministic contribution log passes 2^31 entries
