@@ -452,6 +452,9 @@ __global__ void __launch_bounds__(256, 4) k_lookup_bench(int32_t n, DLib L, cons
 #ifndef EMC_SCORE_BFLY
 #define EMC_SCORE_BFLY 1
 #endif
+#ifndef EMC_SCORE_ACC
+#define EMC_SCORE_ACC 1
+#endif
 __device__ __forceinline__ void score_bins(double* bins, bool valid, int32_t base, const double v[5])
 {
     unsigned todo = __ballot_sync(kFull, valid);
@@ -567,6 +570,10 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
         }
         bool seg = valid;                    // this lane flies a segment this round
         bool moved = false;
+        // fast-mode scores of a chain accumulate per lane while the region
+        // stays and go out in one warp reduction after the chain (EMC_SCORE_ACC)
+        double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        int32_t acc_base = -1;
         for (int rep = 0;; ++rep) {
             double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
             int32_t base = 0;
@@ -668,7 +675,24 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
                     }
                 }
             } else if (bp.score) {
-                score_bins(bins, scored, base, v);
+                if (EMC_SCORE_ACC) {
+                    const bool flush = scored && acc_base >= 0 && base != acc_base;   // region changed
+                    if (__any_sync(kFull, flush)) {
+                        score_bins(bins, flush, acc_base, acc);
+                        if (flush) {
+                            #pragma unroll
+                            for (int k = 0; k < 5; ++k) acc[k] = 0.0;
+                            acc_base = -1;
+                        }
+                    }
+                    if (scored) {
+                        #pragma unroll
+                        for (int k = 0; k < 5; ++k) acc[k] = __dadd_rn(acc[k], v[k]);
+                        acc_base = base;
+                    }
+                } else {
+                    score_bins(bins, scored, base, v);
+                }
             }
             if (__popc(__ballot_sync(kFull, again)) < kChainMinLanes) {
                 if (again) { to_col = false; to_cross = true; }   // back to the lookup queue instead
@@ -682,6 +706,7 @@ __global__ void __launch_bounds__(256, EMC_ADV_MINB) k_advance(const int32_t* __
             }
             seg = again;
         }
+        if (EMC_SCORE_ACC && bp.score && !bp.use_logs) score_bins(bins, acc_base >= 0, acc_base, acc);
         if (moved) { PState& p = S.ps[s]; p.a = a; p.b = b; }
         if (to_col || to_cross) st_p3(&S.ps[s].d, d);
         const bool to_next = to_cross && !leak;
