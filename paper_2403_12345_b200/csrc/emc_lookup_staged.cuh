@@ -769,7 +769,15 @@ __global__ void __launch_bounds__(NW * 32, MINB)
             const int32_t bu = mine ? bin : bs;
             const int32_t mu = mine ? m : ms;
             double st = 0.0, sc = 0.0, sf = 0.0, snf = 0.0;
+// fast-path bracket compares: FP64 compares of the header energies (1) or
+// integer compares of their bit patterns (0); identical for the positive
+// finite grid energies here; measured lookup -0.7% with FP64 (fewer live
+// registers around the header loads)
+#ifndef EMC_LK_HDR_F64
+#define EMC_LK_HDR_F64 1
+#endif
             const long long Eb = __double_as_longlong(Eu);
+            (void)Eb;
             // checkpoint rows this lane stores in this pass: row r (after
             // nuclide (r+1)*stride) exists iff (r+1)*stride <= ncomp and r < nck;
             // one compare per checkpoint instead of (ckon, mine, ncomp, nck)
@@ -787,7 +795,12 @@ __global__ void __launch_bounds__(NW * 32, MINB)
 #pragma unroll
                     for (int j = 0; j < LK_G; ++j) {
                         const longlong2 ab = sh.hdr[d][j];
+#if EMC_LK_HDR_F64
+                        lis |= ((uint32_t)(__longlong_as_double(ab.x) <= Eu) +
+                                (uint32_t)(__longlong_as_double(ab.y) <= Eu)) << (2 * j);
+#else
                         lis |= ((uint32_t)(ab.x <= Eb) + (uint32_t)(ab.y <= Eb)) << (2 * j);
+#endif
                     }
 #pragma unroll kLkFastUnroll
                     for (int j = 0; j < LK_G; ++j) {
