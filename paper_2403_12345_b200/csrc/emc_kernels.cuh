@@ -530,14 +530,15 @@ __device__ __forceinline__ void cross_surface(P0& a, P1& b, P3& d, const DGeom& 
 // very same macroscopic cross sections (same material, same energy; the slot's
 // sigma_t checkpoints were written by that same lookup and the slot does not
 // move inside this kernel), so the particle takes its next flight here, up to
-// kMaxChain segments per launch (2: one chained flight; longer chains keep
-// whole warps waiting on a few lanes -- measured, C4 +4.5%, C3 +4% at 2, worse
-// beyond 3).  The skipped lookups are counted as the
+// kMaxChain segments per launch (3 since the chain's scores are reduced once
+// per chain: C4 +1.6%, C3 +2.6%, C2 +6.6% over 2; 4 and 6 segments, or a
+// minimum of 4 / 8 chaining lanes per warp, are not better; before the
+// accumulation 2 was best: C4 +4.5% over no chains).  The skipped lookups are counted as the
 // lookup events (and interpolations) they are in the reference; draws,
 // scores, log ordinals and banked sites are exactly those of the unchained
 // schedule (physics is schedule-invariant, acceptance criterion 1).
 #ifndef EMC_ADV_CHAIN
-#define EMC_ADV_CHAIN 2
+#define EMC_ADV_CHAIN 3
 #endif
 constexpr int kMaxChain = EMC_ADV_CHAIN;
 #ifndef EMC_ADV_CHAIN_MIN
